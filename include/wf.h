@@ -1,0 +1,153 @@
+/* wf.h -- C ABI of the B200-native WallFacer multi-ring attention library (libwf.so).
+ *
+ * WallFacer (arXiv 2407.00611) shards one sequence of N tokens over P GPUs, groups
+ * them into P/C teams of C (§3.2.1), team-gathers Q/K/V, passes K/V
+ * blocks along C^2 sub-rings of length P/C^2 (Alg. 1; Alg. 2/3,
+ * PAPER.md:263-292) and merges the C partial (O, lse) results of a team with an
+ * LSE-weighted reduce-scatter (Alg. 1 l.11).  The backward keeps K/V
+ * and dK/dV stationary and circulates the queries with dQ.
+ * At C = 1 the same calls are plain Ring Attention.
+ *
+ * Conventions (all calls):
+ *  - One process per GPU.  All pointers are DEVICE pointers owned by the caller
+ *    unless stated; nothing is freed or retained by the library after a call returns
+ *    except the context's own workspace.
+ *  - Tensors are contiguous [tokens, heads, head_dim] bf16 (B = 1),
+ *    rows 16-byte aligned.  LSE is fp32 [heads, tokens], natural log (reading c16).
+ *  - Causal inputs are the caller's ZIGZAG shard: rank r passes chunk r followed by
+ *    chunk 2P-1-r of the 2P equal chunks (reading c13); full-mask inputs
+ *    are the contiguous shard [r N/P, (r+1) N/P).  wf_shard_ranges
+ *    returns these ranges.
+ *  - Work is enqueued on `stream` and the call returns after enqueue; internal streams
+ *    are joined back into `stream` before return.  Every rank calls collectively with
+ *    identical (N, heads, head_dim, causal).
+ *  - Errors: every call returns a wf_status; wf_last_error(ctx) gives the text.
+ *    WF_ERR_CONFIG: invalid (P, C) or unsupported shape (head_dim not in {64, 72, 128};
+ *    N not a multiple of 128 P (full) or 256 P (causal)).  WF_ERR_ARG: null or
+ *    misaligned pointer.  WF_ERR_CUDA / WF_ERR_COMM: a CUDA or NCCL failure; the
+ *    context should then be finalized.  (Mirrors SPEC.md:524 exit codes 0/1/2.)
+ */
+#ifndef WF_H_
+#define WF_H_
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wf_ctx wf_ctx; /* opaque: plan, communicators, workspace, streams, trace */
+
+typedef enum {
+  WF_OK = 0,
+  WF_ERR_NUMERIC = 1, /* harness-level only (tolerance / trace mismatch) */
+  WF_ERR_CONFIG = 2,
+  WF_ERR_ARG = 3,
+  WF_ERR_CUDA = 4,
+  WF_ERR_COMM = 5
+} wf_status;
+
+typedef enum {
+  WF_TOPO_COLLECT_INTRA = 0, /* teams contiguous in rank: Alg. 2's placement */
+  WF_TOPO_P2P_INTRA = 1      /* accepted; identical on one NVSwitch node      */
+} wf_topology;
+
+/* Opaque 128-byte id wrapping an ncclUniqueId.  Rank 0 calls wf_get_uid and the
+ * caller broadcasts the bytes (e.g. torch.distributed) to every rank before wf_init. */
+typedef struct {
+  uint8_t bytes[128];
+} wf_uid;
+
+/* One CommTrace record (SURVEY.md §8(c) "Oracle schedule simulator"): pass 0 = forward,
+ * 1 = backward; kind is a WF_KIND_* value; step -1 gathers / init shuffle, s in
+ * [0, R-2] ring hop after compute step s, R-1 the dQ return hop, R post-loop reductions;
+ * block = team block, team, or unit id (by kind); bytes on the wire.  Only messages
+ * with src != dst are recorded. */
+typedef struct {
+  int32_t pass, kind, step, src, dst, block;
+  int64_t bytes;
+} wf_event;
+
+enum {
+  WF_KIND_AG_Q = 0, WF_KIND_AG_KV, WF_KIND_INIT_KV, WF_KIND_SLICE_KV, WF_KIND_RING_KV, WF_KIND_RS_O,
+  WF_KIND_RS_LSE, WF_KIND_AG_QDO, WF_KIND_AG_STATS, WF_KIND_RING_QPKG, WF_KIND_RING_DQ, WF_KIND_RET_DQ,
+  WF_KIND_REV_DKV, WF_KIND_RS_DKV, WF_KIND_RS_DQ, WF_KIND_COUNT
+};
+
+/* Rank 0: create the NCCL unique id of a new context.  out: host memory. */
+wf_status wf_get_uid(wf_uid* out);
+
+/* Create this rank's context: validates (P, C) (reading c2: C | P and, when C^2 <= P,
+ * C^2 | P; C^2 > P is the extension regime with R = 1), builds the plan (Alg. 2/3),
+ * creates the NCCL communicator on the current CUDA device.  uid: host memory, the
+ * same bytes on every rank; may be NULL when P == 1.  out: receives the context. */
+wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, wf_ctx** out);
+
+/* Single-GPU emulation of all P ranks (test/bench aid): the same schedule, block
+ * kernels and trace, with every message a device-local copy.  In this mode every
+ * tensor argument of wf_attn_fwd / wf_attn_bwd addresses the P rank shards
+ * concatenated rank-major: [P][N/P, heads, head_dim] (LSE: [P][heads, N/P]). */
+wf_status wf_init_emulated(int P, int C, wf_ctx** out);
+
+/* Forward (Alg. 1): Q, K, V bf16 [N/P, heads, head_dim] (this rank's shard) ->
+ * O bf16 [N/P, heads, head_dim], LSE fp32 [heads, N/P]. */
+wf_status wf_attn_fwd(wf_ctx* ctx, const void* Q, const void* K, const void* V, int64_t N, int heads,
+                      int head_dim, int causal, void* O, float* LSE, void* stream);
+
+/* Backward: given dO and the forward's Q, K, V, O, LSE (same
+ * shapes as wf_attn_fwd) -> dQ, dK, dV bf16 [N/P, heads, head_dim]. */
+wf_status wf_attn_bwd(wf_ctx* ctx, const void* dO, const void* Q, const void* K, const void* V, const void* O,
+                      const float* LSE, int64_t N, int heads, int head_dim, int causal, void* dQ, void* dK,
+                      void* dV, void* stream);
+
+/* Copy the CommTrace of the last forward + backward of this rank (all ranks in
+ * emulated mode) into buf (host memory, cap records).  n_out: records available. */
+wf_status wf_get_trace(wf_ctx* ctx, wf_event* buf, size_t cap, size_t* n_out);
+
+/* Host-only: the trace this library will emit for (P, C, N, heads, head_dim) and one
+ * rank (rank = -1: all ranks), forward and backward, without a GPU or a context.
+ * Same record semantics as wf_get_trace. */
+wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,
+                        size_t* n_out);
+
+/* Host-only: the plan of one rank: out[0..5] = {init_send, init_recv, next, last, R, regime}
+ * (regime 0 = paper, 1 = extension). */
+wf_status wf_plan(int P, int C, int rank, int32_t out[6]);
+
+/* Host-only: global token ranges of rank's shard: ranges[0..3] =
+ * {a0, a1, b0, b1}, the shard being [a0, a1) followed by [b0, b1) (b0 == b1 when full). */
+wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges[4]);
+
+/* Timing aid: number of kernels this context launched since creation. */
+int64_t wf_kernel_launches(const wf_ctx* ctx);
+
+/* Last error text of ctx (or of the last context-less call when ctx is NULL). */
+const char* wf_last_error(const wf_ctx* ctx);
+
+/* Destroy the context: frees workspace, communicators, streams. */
+wf_status wf_finalize(wf_ctx* ctx);
+
+/* ---- per-step kernels, exported for parity tests of one ring step ---------------
+ * wf_block_fwd: PAPER.md:183 forward_iteration on one device.  q [nq, heads, D],
+ * k/v [nk, heads, D] bf16; positions: row r of q sits at global token
+ * qstart[r / chunk] + r % chunk (likewise k); chunk multiple of 128 (ignored unless
+ * causal).  o_in/lse_in: optional fp32 state (NULL = empty state, lse = -inf).
+ * Writes fp32 o_out (if non-NULL), bf16 o_bf16 (if non-NULL) and lse_out [heads, nq]. */
+wf_status wf_block_fwd(const void* q, const void* k, const void* v, int nq, int nk, int heads, int head_dim,
+                       int causal, int chunk, const int32_t* qstart, int nqchunks, const int32_t* kstart,
+                       int nkchunks, const float* o_in, const float* lse_in, float* o_out, void* o_bf16,
+                       float* lse_out, void* stream);
+
+/* wf_block_bwd: PAPER.md:203 one flash-attention backward step: the K/V block
+ * (stationary) against query rows q with dO, final LSE and D = rowsum(dO o O) [heads, nq].
+ * dq_acc fp32 [nq, heads, D] is accumulated (+=) atomically; dk_acc/dv_acc fp32
+ * [nk, heads, D] are accumulated when accumulate != 0, else overwritten. */
+wf_status wf_block_bwd(const void* q, const void* k, const void* v, const void* dO, const float* lse,
+                       const float* dsum, int nq, int nk, int heads, int head_dim, int causal, int chunk,
+                       const int32_t* qstart, int nqchunks, const int32_t* kstart, int nkchunks, float* dq_acc,
+                       float* dk_acc, float* dv_acc, int accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WF_H_ */

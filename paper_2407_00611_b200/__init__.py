@@ -1,0 +1,6 @@
+"""B200-native WallFacer multi-ring attention (arXiv 2407.00611).
+
+The product is libwf.so (C ABI, include/wf.h) built from csrc/; this package is
+its thin Python binding.  See DESIGN.md.
+"""
+from .wf import Context, WFError, block_bwd, block_fwd, plan, plan_trace, shard_ranges  # noqa: F401

@@ -1,0 +1,135 @@
+// blocks_api.cu -- TMA map encoding and the exported per-step kernel entry points
+// (wf_block_fwd / wf_block_bwd of include/wf.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/wf.h"
+#include "common.h"
+#include "internal.h"
+
+namespace wf {
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(heads) * D * 2};
+  cuuint32_t box[3] = {64, 1, WF_TILE};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool fill_postable(PosTable* t, int rows, int chunk, const int32_t* starts, int n) {
+  std::memset(t, 0, sizeof(*t));
+  if (chunk <= 0) {  // contiguous [0, rows)
+    t->chunk = rows;
+    t->nchunks = 1;
+    t->start[0] = 0;
+    return true;
+  }
+  if (chunk % WF_TILE || n <= 0 || n > WF_MAX_CHUNKS || static_cast<int64_t>(n) * chunk != rows) return false;
+  t->chunk = chunk;
+  t->nchunks = n;
+  for (int i = 0; i < n; ++i) t->start[i] = starts[i];
+  return true;
+}
+
+}  // namespace wf
+
+using namespace wf;
+
+static thread_local char g_err[512];
+const char* wf_static_error() { return g_err; }
+static wf_status set_err(wf_status s, const char* msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg);
+  return s;
+}
+
+extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, int nq, int nk, int heads,
+                                  int head_dim, int causal, int chunk, const int32_t* qstart, int nqchunks,
+                                  const int32_t* kstart, int nkchunks, const float* o_in, const float* lse_in,
+                                  float* o_out, void* o_bf16, float* lse_out, void* stream) {
+  if (!q || !k || !v || !lse_out || (!o_out && !o_bf16)) return set_err(WF_ERR_ARG, "wf_block_fwd: null pointer");
+  if ((o_in == nullptr) != (lse_in == nullptr)) return set_err(WF_ERR_ARG, "wf_block_fwd: o_in/lse_in must pair");
+  if (nq <= 0 || nq % WF_TILE || nk < 0 || nk % WF_TILE) return set_err(WF_ERR_CONFIG, "wf_block_fwd: nq, nk must be multiples of 128");
+  if (head_dim != 64 && head_dim != 72 && head_dim != 128) return set_err(WF_ERR_CONFIG, "wf_block_fwd: head_dim not in {64,72,128}");
+  FwdArgs a{};
+  a.nq = nq;
+  a.nk = nk;
+  a.heads = heads;
+  a.causal = causal;
+  if (causal) {
+    if (!fill_postable(&a.qpos, nq, chunk, qstart, nqchunks) || !fill_postable(&a.kpos, nk, chunk, kstart, nkchunks))
+      return set_err(WF_ERR_CONFIG, "wf_block_fwd: bad chunk table");
+  }
+  a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(head_dim));
+  a.o_in = o_in;
+  a.lse_in = lse_in;
+  a.o_out_f32 = o_out;
+  a.o_out_bf16 = static_cast<__nv_bfloat16*>(o_bf16);
+  a.lse_out = lse_out;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_rows(&tq, q, nq, heads, head_dim) || !make_tmap_rows(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim) ||
+      !make_tmap_rows(&tv, v, nk > 0 ? nk : WF_TILE, heads, head_dim))
+    return set_err(WF_ERR_ARG, "wf_block_fwd: TMA map encode failed (alignment?)");
+  cudaError_t e = launch_block_fwd(tq, tk, tv, a, head_dim, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
+  return WF_OK;
+}
+
+extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, const void* dO, const float* lse,
+                                  const float* dsum, int nq, int nk, int heads, int head_dim, int causal, int chunk,
+                                  const int32_t* qstart, int nqchunks, const int32_t* kstart, int nkchunks,
+                                  float* dq_acc, float* dk_acc, float* dv_acc, int accumulate, void* stream) {
+  if (!q || !k || !v || !dO || !lse || !dsum || !dq_acc || !dk_acc || !dv_acc)
+    return set_err(WF_ERR_ARG, "wf_block_bwd: null pointer");
+  if (nq < 0 || nq % WF_TILE || nk <= 0 || nk % WF_TILE) return set_err(WF_ERR_CONFIG, "wf_block_bwd: nq, nk must be multiples of 128");
+  if (head_dim != 64 && head_dim != 72 && head_dim != 128) return set_err(WF_ERR_CONFIG, "wf_block_bwd: head_dim not in {64,72,128}");
+  BwdArgs a{};
+  a.nq = nq;
+  a.nk = nk;
+  a.heads = heads;
+  a.causal = causal;
+  if (causal) {
+    if (!fill_postable(&a.qpos, nq, chunk, qstart, nqchunks) || !fill_postable(&a.kpos, nk, chunk, kstart, nkchunks))
+      return set_err(WF_ERR_CONFIG, "wf_block_bwd: bad chunk table");
+  }
+  a.scale = 1.f / std::sqrt(static_cast<float>(head_dim));
+  a.scale_log2 = 1.4426950408889634f * a.scale;
+  a.lse = lse;
+  a.dsum = dsum;
+  a.dq_acc = dq_acc;
+  a.dk_acc = dk_acc;
+  a.dv_acc = dv_acc;
+  a.dkv_accumulate = accumulate;
+  CUtensorMap tq, tk, tv, tdo;
+  if (!make_tmap_rows(&tq, q, nq > 0 ? nq : WF_TILE, heads, head_dim) || !make_tmap_rows(&tk, k, nk, heads, head_dim) ||
+      !make_tmap_rows(&tv, v, nk, heads, head_dim) || !make_tmap_rows(&tdo, dO, nq > 0 ? nq : WF_TILE, heads, head_dim))
+    return set_err(WF_ERR_ARG, "wf_block_bwd: TMA map encode failed (alignment?)");
+  cudaError_t e = launch_block_bwd(tq, tk, tv, tdo, a, head_dim, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
+  return WF_OK;
+}

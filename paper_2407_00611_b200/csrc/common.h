@@ -1,0 +1,86 @@
+// common.h -- host/device shared definitions of the WallFacer B200 library.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#define WF_MAX_CHUNKS 32
+#define WF_TILE 128
+
+namespace wf {
+
+// Global-position table of a row buffer made of equal chunks (zigzag halves or
+// whole units).  Row r of the buffer sits at global token
+//   start[r / chunk] + r % chunk.
+// chunk is a multiple of WF_TILE, so every 128-row tile is one contiguous range.
+struct PosTable {
+  int chunk;                      // rows per chunk (multiple of 128)
+  int nchunks;
+  int start[WF_MAX_CHUNKS];       // global start of each chunk
+};
+
+// Arguments of one block-forward launch (PAPER.md:183 forward_iteration):
+// the (O, lse) state of the query rows is merged with attention against one K/V block.
+struct FwdArgs {
+  int nq, nk, heads;
+  int causal;
+  PosTable qpos, kpos;
+  float scale_log2;               // log2(e) / sqrt(head_dim)
+  const float* o_in;              // optional state: fp32 [nq, heads, D] (normalised O)
+  const float* lse_in;            // optional state: fp32 [heads, nq] natural log
+  float* o_out_f32;               // state out (fp32) or null
+  __nv_bfloat16* o_out_bf16;      // final out (bf16) or null
+  float* lse_out;                 // [heads, nq]
+};
+
+// Arguments of one block-backward launch (flash-attention backward):
+// the stationary K/V block accumulates dK/dV, the travelling query rows accumulate dQ.
+struct BwdArgs {
+  int nq, nk, heads;
+  int causal;
+  PosTable qpos, kpos;
+  float scale_log2;               // log2(e) / sqrt(head_dim)
+  float scale;                    // 1 / sqrt(head_dim)
+  const float* lse;               // [heads, nq] natural-log LSE of the query rows (final forward)
+  const float* dsum;              // [heads, nq] D = rowsum(dO o O)
+  float* dq_acc;                  // fp32 [nq, heads, D] accumulated with atomics
+  float* dk_acc;                  // fp32 [nk, heads, D] (accumulate if dkv_accumulate)
+  float* dv_acc;
+  __nv_bfloat16* dk_out;          // if non-null: write bf16 dK (and dV) instead of fp32 acc
+  __nv_bfloat16* dv_out;
+  int dkv_accumulate;             // 1: dk_acc += ; 0: dk_acc =
+};
+
+// Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.
+bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
+
+cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
+                             int D, cudaStream_t s);
+cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                             const CUtensorMap& tdo, const BwdArgs& a, int D, cudaStream_t s);
+
+}  // namespace wf
+
+#define WF_MAX_PARTS 8
+namespace wf {
+// ReduceScatter_combine of the C partial (O, lse) states of this rank's rows.
+struct MergeArgs {
+  int rows, heads, D, nparts;
+  const __nv_bfloat16* o[WF_MAX_PARTS];   // [rows, heads, D] each
+  const float* lse[WF_MAX_PARTS];         // lse[j][head * lse_stride[j] + row]
+  int64_t lse_stride[WF_MAX_PARTS];
+  __nv_bfloat16* out;                     // [rows, heads, D]
+  float* lse_out;                         // [heads, rows]
+};
+struct SumArgs {
+  int64_t n;                              // elements (multiple of 4)
+  int nparts;
+  const float* parts[WF_MAX_PARTS];
+  __nv_bfloat16* out;
+};
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
+cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* dsum, int rows, int heads, int D,
+                        cudaStream_t s);
+cudaError_t launch_sum(const SumArgs& a, cudaStream_t s);
+}  // namespace wf

@@ -1,0 +1,155 @@
+// reduce.cu -- HBM-bound kernels around the block kernels:
+//   * wf_merge_kernel  : Alg. 1 l.11 ReduceScatter_combine:
+//                        L = logsumexp_a lse_a, O = sum_a exp(lse_a - L) O_a over the C
+//                        partials of this rank's rows -> bf16 O, fp32 LSE.
+//   * wf_dsum_kernel   : D = rowsum(dO o O) (flash-attention backward preprocess; reading c12).
+//   * wf_sum_kernel    : the backward team reductions (reading c11): out = sum_j part_j
+//                        (fp32 partials -> bf16).
+// All are bandwidth kernels: 16-byte vector loads/stores, grid-stride, grid sized from
+// the SM count.
+#include "common.h"
+#include "internal.h"
+
+namespace wf {
+
+namespace {
+
+__device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+
+// One thread = 8 contiguous elements (16 B of bf16) of one (row, head).
+__global__ void wf_merge_kernel(MergeArgs a) {
+  const int64_t per_row = a.heads * a.D / 8;  // 8-element groups per token row
+  const int64_t total = static_cast<int64_t>(a.rows) * per_row;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(g / per_row);
+    const int e0 = static_cast<int>(g % per_row) * 8;
+    const int head = e0 / a.D;
+    float l[WF_MAX_PARTS];
+    float L = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < WF_MAX_PARTS; ++j) {
+      if (j < a.nparts) {
+        l[j] = a.lse[j][static_cast<int64_t>(head) * a.lse_stride[j] + row];
+        L = fmaxf(L, l[j]);
+      }
+    }
+    float s = 0.f;
+    if (L != -INFINITY) {
+#pragma unroll
+      for (int j = 0; j < WF_MAX_PARTS; ++j)
+        if (j < a.nparts) s += __expf(l[j] - L);
+    }
+    const float Lf = (L == -INFINITY) ? -INFINITY : L + __logf(s);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (L != -INFINITY) {
+#pragma unroll
+      for (int j = 0; j < WF_MAX_PARTS; ++j) {
+        if (j < a.nparts && l[j] != -INFINITY) {
+          const float w = __expf(l[j] - Lf);
+          const uint4 v = *reinterpret_cast<const uint4*>(a.o[j] + static_cast<int64_t>(row) * a.heads * a.D + e0);
+          const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fmaf(w, bf2f(h[i]), acc[i]);
+        }
+      }
+    }
+    uint4 out;
+    uint32_t* po = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      po[i] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    *reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row) * a.heads * a.D + e0) = out;
+    if (e0 % a.D == 0) a.lse_out[static_cast<int64_t>(head) * a.rows + row] = Lf;
+  }
+}
+
+// D[h][row] = sum_d dO[row,h,d] * O[row,h,d]; one 8-lane group per (row, head).
+__global__ void wf_dsum_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
+                               float* __restrict__ dsum, int rows, int heads, int D) {
+  const int lanes = 8;
+  const int64_t total = static_cast<int64_t>(rows) * heads;
+  const int sub = threadIdx.x % lanes;
+  for (int64_t g = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / lanes; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x / lanes) {
+    const int row = static_cast<int>(g / heads);
+    const int head = static_cast<int>(g % heads);
+    const int64_t base = (static_cast<int64_t>(row) * heads + head) * D;
+    float acc = 0.f;
+    for (int e = sub * 8; e < D; e += lanes * 8) {
+      const uint4 x = *reinterpret_cast<const uint4*>(dO + base + e);
+      const uint4 y = *reinterpret_cast<const uint4*>(O + base + e);
+      const uint16_t* hx = reinterpret_cast<const uint16_t*>(&x);
+      const uint16_t* hy = reinterpret_cast<const uint16_t*>(&y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(bf2f(hx[i]), bf2f(hy[i]), acc);
+    }
+#pragma unroll
+    for (int o = lanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
+    if (sub == 0) dsum[static_cast<int64_t>(head) * rows + row] = acc;
+  }
+}
+
+// out[i] = bf16(sum_j part_j[i]), 4 elements per thread.
+__global__ void wf_sum_kernel(SumArgs a) {
+  const int64_t n4 = a.n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < WF_MAX_PARTS; ++j) {
+      if (j < a.nparts) {
+        const float4 v = reinterpret_cast<const float4*>(a.parts[j])[i];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y), hi = __floats2bfloat162_rn(s.z, s.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&lo);
+    o.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(a.out)[i] = o;
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(nsm) * 8;
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
+  if (a.D % 8 || a.nparts < 1 || a.nparts > WF_MAX_PARTS) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(a.rows) * a.heads * a.D / 8;
+  wf_merge_kernel<<<grid_for(work, 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* dsum, int rows, int heads, int D,
+                        cudaStream_t s) {
+  if (D % 8) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(rows) * heads * 8;
+  wf_dsum_kernel<<<grid_for(work, 256), 256, 0, s>>>(dO, O, dsum, rows, heads, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum(const SumArgs& a, cudaStream_t s) {
+  if (a.n % 4 || a.nparts < 1 || a.nparts > WF_MAX_PARTS) return cudaErrorInvalidValue;
+  wf_sum_kernel<<<grid_for(a.n / 4, 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace wf

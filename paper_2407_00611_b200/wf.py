@@ -1,0 +1,165 @@
+"""Thin torch-facing binding of libwf.so (argument marshalling only).
+
+Every step of the hot path runs inside libwf.so's CUDA kernels; torch supplies
+device memory, streams and (for multi-GPU) the process group that broadcasts
+the NCCL id.  Names follow include/wf.h.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import KINDS, WfEvent, WfUid, lib
+
+__all__ = ["WFError", "block_fwd", "block_bwd", "Context", "plan", "plan_trace", "shard_ranges"]
+
+
+class WFError(RuntimeError):
+    pass
+
+
+def _check(st, ctx=None):
+    if st != 0:
+        msg = lib().wf_last_error(ctx)
+        raise WFError(f"wf status {st}: {msg.decode() if msg else ''}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise WFError("tensor arguments must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _i32arr(xs):
+    if xs is None:
+        return None, 0
+    arr = (ctypes.c_int32 * len(xs))(*[int(x) for x in xs])
+    return arr, len(xs)
+
+
+def _bf16(t, name):
+    if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+        raise WFError(f"{name}: need a contiguous CUDA bf16 tensor")
+    return t
+
+
+def block_fwd(q, k, v, causal=False, chunk=0, qstart=None, kstart=None, o_in=None, lse_in=None,
+              out_f32=False, out_bf16=True):
+    """One forward_iteration on the current device: returns (o_f32|None, o_bf16|None, lse)."""
+    nq, h, d = q.shape
+    nk = k.shape[0]
+    of = torch.empty((nq, h, d), dtype=torch.float32, device=q.device) if out_f32 else None
+    ob = torch.empty((nq, h, d), dtype=torch.bfloat16, device=q.device) if out_bf16 else None
+    lse = torch.empty((h, nq), dtype=torch.float32, device=q.device)
+    qs, nqs = _i32arr(qstart)
+    ks, nks = _i32arr(kstart)
+    _check(lib().wf_block_fwd(_ptr(_bf16(q, "q")), _ptr(_bf16(k, "k")), _ptr(_bf16(v, "v")), nq, nk, h, d,
+                              int(causal), int(chunk), qs, nqs, ks, nks, _ptr(o_in), _ptr(lse_in), _ptr(of), _ptr(ob),
+                              _ptr(lse), _stream()))
+    return of, ob, lse
+
+
+def block_bwd(q, k, v, do, lse, dsum, dq_acc, dk_acc, dv_acc, causal=False, chunk=0, qstart=None, kstart=None,
+              accumulate=False):
+    """One flash-attention backward step on the current device (in place on the accumulators)."""
+    nq, h, d = q.shape
+    nk = k.shape[0]
+    qs, nqs = _i32arr(qstart)
+    ks, nks = _i32arr(kstart)
+    _check(lib().wf_block_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(do), _ptr(lse), _ptr(dsum), nq, nk, h, d, int(causal),
+                              int(chunk), qs, nqs, ks, nks, _ptr(dq_acc), _ptr(dk_acc), _ptr(dv_acc), int(accumulate),
+                              _stream()))
+
+
+def plan(P, C, rank):
+    out = (ctypes.c_int32 * 6)()
+    _check(lib().wf_plan(P, C, rank, out))
+    return dict(send=out[0], recv=out[1], next=out[2], last=out[3], R=out[4], regime="paper" if out[5] == 0 else "ext")
+
+
+def _events(buf, n):
+    return [(e.pas, KINDS[e.kind], e.step, e.src, e.dst, e.block, e.nbytes) for e in buf[:n]]
+
+
+def plan_trace(P, C, N, heads, head_dim, rank=-1):
+    n = ctypes.c_size_t(0)
+    _check(lib().wf_plan_trace(P, C, N, heads, head_dim, rank, None, 0, ctypes.byref(n)))
+    buf = (WfEvent * max(1, n.value))()
+    _check(lib().wf_plan_trace(P, C, N, heads, head_dim, rank, buf, n.value, ctypes.byref(n)))
+    return _events(buf, n.value)
+
+
+def shard_ranges(P, rank, N, causal):
+    out = (ctypes.c_int64 * 4)()
+    _check(lib().wf_shard_ranges(P, rank, N, int(causal), out))
+    return list(out)
+
+
+class Context:
+    """A wf_ctx: real (one rank of a torch.distributed job) or emulated (all P ranks on one GPU)."""
+
+    def __init__(self, P, C, rank=0, emulated=False, group=None, topology=0):
+        self.P, self.C, self.rank, self.emulated = P, C, rank, emulated
+        h = ctypes.c_void_p()
+        if emulated:
+            _check(lib().wf_init_emulated(P, C, ctypes.byref(h)))
+        else:
+            uid = WfUid()
+            if P > 1:
+                import torch.distributed as dist
+                if rank == 0:
+                    _check(lib().wf_get_uid(ctypes.byref(uid)))
+                t = torch.tensor(list(bytes(uid.bytes)), dtype=torch.uint8)
+                if dist.get_backend(group) == "nccl":
+                    t = t.cuda()
+                dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+                for i, b in enumerate(t.cpu().tolist()):
+                    uid.bytes[i] = b
+            _check(lib().wf_init(P, C, topology, rank, ctypes.byref(uid), ctypes.byref(h)))
+        self.h = h
+
+    def fwd(self, q, k, v, N, causal, o=None, lse=None):
+        rows, h, d = q.shape
+        o = torch.empty_like(q) if o is None else o
+        lse_shape = (self.P, h, rows // self.P) if self.emulated else (h, rows)
+        lse = torch.empty(lse_shape, dtype=torch.float32, device=q.device) if lse is None else lse
+        _check(lib().wf_attn_fwd(self.h, _ptr(q), _ptr(k), _ptr(v), N, h, d, int(causal), _ptr(o), _ptr(lse),
+                                 _stream()), self.h)
+        return o, lse
+
+    def bwd(self, do, q, k, v, o, lse, N, causal, dq=None, dk=None, dv=None):
+        rows, h, d = q.shape
+        dq = torch.empty_like(q) if dq is None else dq
+        dk = torch.empty_like(k) if dk is None else dk
+        dv = torch.empty_like(v) if dv is None else dv
+        _check(lib().wf_attn_bwd(self.h, _ptr(do), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), N, h, d,
+                                 int(causal), _ptr(dq), _ptr(dk), _ptr(dv), _stream()), self.h)
+        return dq, dk, dv
+
+    def trace(self):
+        n = ctypes.c_size_t(0)
+        _check(lib().wf_get_trace(self.h, None, 0, ctypes.byref(n)), self.h)
+        buf = (WfEvent * max(1, n.value))()
+        _check(lib().wf_get_trace(self.h, buf, n.value, ctypes.byref(n)), self.h)
+        return _events(buf, n.value)
+
+    def kernel_launches(self):
+        return int(lib().wf_kernel_launches(self.h))
+
+    def close(self):
+        if self.h:
+            lib().wf_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

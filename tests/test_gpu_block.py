@@ -1,0 +1,131 @@
+"""GPU parity of the per-ring-step block kernels (through the C ABI) vs the fp64 oracle.
+
+Tolerances (north_star, BASELINE.json): O max-abs <= 2e-2; dQ/dK/dV max-abs
+normalised by max|ref| <= 2e-2; advisory LSE max-abs <= 1e-2 (checked).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.blocks import block_bwd as o_block_bwd
+from oracle.dense import attention_fwd
+from wf_inputs import make_qkv_do, to_f64
+
+pytestmark = pytest.mark.gpu
+
+O_TOL = 2e-2
+LSE_TOL = 1e-2
+G_TOL = 2e-2
+
+
+def _wf():
+    import paper_2407_00611_b200 as wf
+    return wf
+
+
+def _pos(chunk, starts):
+    return np.concatenate([np.arange(s, s + chunk) for s in starts])
+
+
+def _run_fwd(N_q, N_k, h, d, causal, chunk, qstart, kstart, seed=0, peaky=False):
+    wf = _wf()
+    q, k, v, _ = make_qkv_do(max(N_q, N_k), h, d, seed=seed, peaky=peaky)
+    q, k, v = q[:N_q], k[:N_k], v[:N_k]
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    _, ob, lse = wf.block_fwd(qd, kd, vd, causal=causal, chunk=chunk, qstart=qstart, kstart=kstart)
+    torch.cuda.synchronize()
+    qp = _pos(chunk, qstart) if causal else np.arange(N_q)
+    kp = _pos(chunk, kstart) if causal else np.arange(N_k)
+    o_ref, l_ref = attention_fwd(to_f64(q), to_f64(k), to_f64(v), qp, kp, causal)
+    return to_f64(ob), lse.cpu().double().numpy(), o_ref, l_ref
+
+
+def _cmp_lse(l, lr):
+    fin = np.isfinite(lr)
+    assert np.array_equal(np.isfinite(l), fin)
+    return np.abs(l[fin] - lr[fin]).max() if fin.any() else 0.0
+
+
+@pytest.mark.parametrize("d", [128, 64, 72])
+@pytest.mark.parametrize("peaky", [False, True])
+def test_block_fwd_full(d, peaky):
+    o, l, o_ref, l_ref = _run_fwd(384, 512, 2, d, False, 0, None, None, peaky=peaky)
+    eo = np.abs(o - o_ref).max()
+    el = _cmp_lse(l, l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+@pytest.mark.parametrize("d", [128, 72])
+def test_block_fwd_causal_contiguous(d):
+    o, l, o_ref, l_ref = _run_fwd(1024, 1024, 2, d, True, 1024, [0], [0], peaky=True)
+    eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+def test_block_fwd_causal_zigzag_chunks():
+    # team-style buffers: query chunks and key chunks at scattered global offsets,
+    # including fully masked rows (query chunk before every key chunk).
+    chunk = 256
+    qstart = [0, 1792, 512, 1280]
+    kstart = [256, 1536, 768, 1024]
+    o, l, o_ref, l_ref = _run_fwd(1024, 1024, 3, 128, True, chunk, qstart, kstart, peaky=True)
+    eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_block_fwd_state_merge(causal):
+    """Two ring steps on one device: step 0 writes the fp32 (O, lse) state, step 1 merges."""
+    wf = _wf()
+    h, d, n = 2, 128, 512
+    q, k, v, _ = make_qkv_do(3 * n, h, d, seed=3, peaky=True)
+    qd = q[:n].cuda()
+    chunk = 256
+    qstart = [1024, 256]            # query rows = tokens [1024,1280) + [256,512)
+    blocks = [([0, 512], k[:n], v[:n]), ([768, 1280], k[n:2 * n], v[n:2 * n])]
+    of, lse = None, None
+    for i, (ks, kb, vb) in enumerate(blocks):
+        last = i == len(blocks) - 1
+        of2, ob, lse2 = wf.block_fwd(qd, kb.cuda(), vb.cuda(), causal=causal, chunk=chunk, qstart=qstart, kstart=ks,
+                                     o_in=of, lse_in=lse, out_f32=not last, out_bf16=last)
+        of, lse = of2, lse2
+    torch.cuda.synchronize()
+    qp = _pos(chunk, qstart) if causal else np.arange(n)
+    kp = np.concatenate([_pos(chunk, b[0]) for b in blocks]) if causal else np.arange(2 * n)
+    kk = torch.cat([b[1] for b in blocks])
+    vv = torch.cat([b[2] for b in blocks])
+    o_ref, l_ref = attention_fwd(to_f64(q[:n]), to_f64(kk), to_f64(vv), qp, kp, causal)
+    eo = np.abs(to_f64(ob) - o_ref).max()
+    el = _cmp_lse(lse.cpu().double().numpy(), l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("d", [128, 72])
+def test_block_bwd(causal, d):
+    wf = _wf()
+    h, nq, nk = 2, 512, 384
+    chunk = 128
+    qstart = [512, 0, 896, 128]
+    kstart = [256, 768, 0]
+    q, k, v, do = make_qkv_do(nq, h, d, seed=5, peaky=True)
+    k, v = k[:nk], v[:nk]
+    qp = _pos(chunk, qstart) if causal else np.arange(nq)
+    kp = _pos(chunk, kstart) if causal else np.arange(nk)
+    # the final forward statistics of the query rows are those of this block alone here
+    o_ref, l_ref = attention_fwd(to_f64(q), to_f64(k), to_f64(v), qp, kp, causal)
+    dd = np.ascontiguousarray(np.sum(to_f64(do) * o_ref, axis=2).T)
+    dq_r, dk_r, dv_r = o_block_bwd(to_f64(q), to_f64(k), to_f64(v), to_f64(do), l_ref, dd, qp, kp, causal)
+    dev = torch.device("cuda")
+    lse_t = torch.tensor(l_ref, dtype=torch.float32, device=dev)
+    dd_t = torch.tensor(dd, dtype=torch.float32, device=dev)
+    dq = torch.zeros((nq, h, d), dtype=torch.float32, device=dev)
+    dk = torch.zeros((nk, h, d), dtype=torch.float32, device=dev)
+    dv = torch.zeros((nk, h, d), dtype=torch.float32, device=dev)
+    wf.block_bwd(q.cuda(), k.cuda(), v.cuda(), do.cuda(), lse_t, dd_t, dq, dk, dv, causal=causal, chunk=chunk,
+                 qstart=qstart if causal else None, kstart=kstart if causal else None)
+    torch.cuda.synchronize()
+    errs = {}
+    for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
+        errs[name] = np.abs(got.cpu().double().numpy() - ref).max() / max(np.abs(ref).max(), 1e-30)
+    assert max(errs.values()) <= G_TOL, errs
