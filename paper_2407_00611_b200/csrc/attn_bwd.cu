@@ -128,7 +128,7 @@ __global__ void __maxnreg__(200)
         for (int p = 0; p < Cfg::NP; ++p)
           tma_load_3d(smem + Cfg::OFF_Q + st * Cfg::TILE + p * Cfg::PANEL, &tmQ, &bar[B_QF + st], p * 64, head,
                       it * WF_TILE);
-        const size_t soff = static_cast<size_t>(head) * a.nq + it * WF_TILE;
+        const int64_t soff = stat_index(head, it * WF_TILE, a.heads, a.stat_blk);
         bulk_load(stat + st * 256, a.lse + soff, 512, &bar[B_QF + st]);
         bulk_load(stat + st * 256 + 128, a.dsum + soff, 512, &bar[B_QF + st]);
         if (ii >= 1) mbar_wait(&bar[B_DOE], (ii - 1) & 1);

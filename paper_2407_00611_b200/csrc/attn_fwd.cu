@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(192, 1)
     const size_t orow = (static_cast<size_t>(grow) * a.heads + head) * D;
     float m = -INFINITY, l = 0.f;
     if (has_state) {
-      const float ls = a.lse_in[static_cast<size_t>(head) * a.nq + grow];
+      const float ls = a.lse_in[stat_index(head, grow, a.heads, a.lse_blk)];
       m = ls * kLog2e;
       l = (ls == -INFINITY) ? 0.f : 1.f;
 #pragma unroll
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     const bool have_o = ntiles > 0 || has_state;
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    a.lse_out[static_cast<size_t>(head) * a.nq + grow] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
+    a.lse_out[stat_index(head, grow, a.heads, a.lse_blk)] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
 #pragma unroll
     for (int c = 0; c < DP / 16; ++c) {
       uint32_t r[16];

@@ -91,6 +91,7 @@ extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, i
   a.o_out_f32 = o_out;
   a.o_out_bf16 = static_cast<__nv_bfloat16*>(o_bf16);
   a.lse_out = lse_out;
+  a.lse_blk = nq;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_rows(&tq, q, nq, heads, head_dim) || !make_tmap_rows(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim) ||
       !make_tmap_rows(&tv, v, nk > 0 ? nk : WF_TILE, heads, head_dim))
@@ -125,6 +126,7 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
   a.dk_acc = dk_acc;
   a.dv_acc = dv_acc;
   a.dkv_accumulate = accumulate;
+  a.stat_blk = nq > 0 ? nq : WF_TILE;
   CUtensorMap tq, tk, tv, tdo;
   if (!make_tmap_rows(&tq, q, nq > 0 ? nq : WF_TILE, heads, head_dim) || !make_tmap_rows(&tk, k, nk, heads, head_dim) ||
       !make_tmap_rows(&tv, v, nk, heads, head_dim) || !make_tmap_rows(&tdo, dO, nq > 0 ? nq : WF_TILE, heads, head_dim))

@@ -14,6 +14,13 @@ namespace wf {
 // whole units).  Row r of the buffer sits at global token
 //   start[r / chunk] + r % chunk.
 // chunk is a multiple of WF_TILE, so every 128-row tile is one contiguous range.
+// Index of (head, row) in a per-row statistic stored as [rows/blk][heads][blk]
+// (blk = rows gives the plain [heads, rows] layout; blk = one unit's rows gives the
+// member-major layout of team-gathered statistics).
+__host__ __device__ __forceinline__ int64_t stat_index(int head, int row, int heads, int blk) {
+  return static_cast<int64_t>(row / blk) * heads * blk + static_cast<int64_t>(head) * blk + row % blk;
+}
+
 struct PosTable {
   int chunk;                      // rows per chunk (multiple of 128)
   int nchunks;
@@ -32,6 +39,7 @@ struct FwdArgs {
   float* o_out_f32;               // state out (fp32) or null
   __nv_bfloat16* o_out_bf16;      // final out (bf16) or null
   float* lse_out;                 // [heads, nq]
+  int lse_blk;                    // lse layout: rows in blocks of lse_blk, [nq/blk][heads][blk]
 };
 
 // Arguments of one block-backward launch (flash-attention backward):
@@ -50,6 +58,7 @@ struct BwdArgs {
   __nv_bfloat16* dk_out;          // if non-null: write bf16 dK (and dV) instead of fp32 acc
   __nv_bfloat16* dv_out;
   int dkv_accumulate;             // 1: dk_acc += ; 0: dk_acc =
+  int stat_blk;                   // lse/dsum layout: [nq/blk][heads][blk]
 };
 
 // Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.

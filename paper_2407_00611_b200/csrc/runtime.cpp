@@ -1,0 +1,980 @@
+// runtime.cpp -- the C ABI of include/wf.h: context, workspace, and the WallFacer
+// schedule (forward: Alg. 1; backward: PAPER.md:201-205) driving the
+// sm_100a block kernels and the NVLink transport (NCCL P2P on a comm stream).
+//
+// One schedule implementation serves three modes:
+//   real      : one process per GPU; this rank executes its sends/receives with NCCL
+//               (grouped ncclSend/ncclRecv) and its block kernels; records its sends.
+//   emulated  : all P ranks on this GPU; every message is a device-local copy.
+//   dry       : no GPU work at all; only the CommTrace is produced (wf_plan_trace).
+// Messages of one phase are issued in one global order (ranks ascending), so the
+// per-peer order of NCCL sends and receives always matches.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/wf.h"
+#include "common.h"
+#include "internal.h"
+#include "plan.h"
+
+namespace wf {
+namespace {
+
+typedef __nv_bfloat16 bf16;
+
+struct Geo {
+  int P, C, T, R, W;
+  bool paper, causal;
+  int64_t N;
+  int n, c, h, d;     // n rows per rank; c = chunk rows for position tables
+  int64_t E;          // h * d
+  int Bk;             // rows of the K/V block a rank attends per step (C*n paper, W*n ext)
+};
+
+// Per-rank device workspace (one set per virtual rank in emulated mode).
+struct RankBufs {
+  // forward
+  bf16 *qt = nullptr, *kt = nullptr, *vt = nullptr;  // team Q/K/V (C*n rows)
+  bf16 *rk[2] = {nullptr, nullptr}, *rv[2] = {nullptr, nullptr};  // ring / slice K,V (Bk rows)
+  float *o_state = nullptr, *lse_state = nullptr;    // fp32 (C*n rows), lse [C][h][n]
+  bf16* o_part = nullptr;                            // bf16 partial O (C*n rows)
+  bf16* rs_o = nullptr;                              // [C][n rows] partials of my rows
+  float* rs_lse = nullptr;                           // [C][h][n]
+  // backward
+  float* dsum = nullptr;                             // [h][n]
+  bf16* t_do = nullptr;                              // team dO (C*n rows)
+  float *t_lse = nullptr, *t_dsum = nullptr;         // [C][h][n]
+  bf16 *pq[2] = {nullptr, nullptr}, *pdo[2] = {nullptr, nullptr};
+  float *plse[2] = {nullptr, nullptr}, *pdsum[2] = {nullptr, nullptr}, *pdq[2] = {nullptr, nullptr};
+  float* home_dq = nullptr;                          // C*n rows fp32
+  float *dk_acc = nullptr, *dv_acc = nullptr;        // Bk rows fp32
+  float *rev_k = nullptr, *rev_v = nullptr;          // paper: C*n rows; ext: [T][n rows]
+  float *rsq = nullptr, *rsk = nullptr, *rsv = nullptr;  // [C][n rows]
+};
+
+struct Seg {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+};
+
+struct Xfer {
+  int pass, kind, step, src, dst, block;
+  std::vector<Seg> segs;
+};
+
+}  // namespace
+}  // namespace wf
+
+using namespace wf;
+
+struct wf_ctx {
+  Plan plan;
+  int rank = 0;
+  bool emulated = false, dry = false;
+  int dry_rank = -1;  // dry mode: record only events touching this rank as sender (-1: all)
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // workspace
+  int64_t ws_key[4] = {0, 0, 0, 0};
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::vector<RankBufs> rb;
+  std::vector<wf_event> trace_fwd, trace_bwd;
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_ctxless_err;
+
+wf_status fail(wf_ctx* c, wf_status s, const std::string& msg) {
+  if (c)
+    c->err = msg;
+  else
+    g_ctxless_err = msg;
+  return s;
+}
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return fail(ctx, WF_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+#define NCK(x)                                                                                   \
+  do {                                                                                           \
+    ncclResult_t r_ = (x);                                                                       \
+    if (r_ != ncclSuccess) return fail(ctx, WF_ERR_COMM, std::string(#x ": ") + ncclGetErrorString(r_)); \
+  } while (0)
+#define WCK(x)                      \
+  do {                              \
+    wf_status s_ = (x);             \
+    if (s_ != WF_OK) return s_;     \
+  } while (0)
+
+bool local(const wf_ctx* ctx, int r) { return ctx->emulated || (!ctx->dry && r == ctx->rank); }
+bool recorded(const wf_ctx* ctx, int src) {
+  if (ctx->dry) return ctx->dry_rank < 0 || src == ctx->dry_rank;
+  return ctx->emulated || src == ctx->rank;
+}
+
+wf_status check_shape(wf_ctx* ctx, int64_t N, int heads, int head_dim, int causal, Geo* g) {
+  const Plan& p = ctx->plan;
+  if (head_dim != 64 && head_dim != 72 && head_dim != 128)
+    return fail(ctx, WF_ERR_CONFIG, "head_dim must be 64, 72 or 128");
+  if (heads < 1) return fail(ctx, WF_ERR_CONFIG, "heads must be >= 1");
+  const int64_t q = causal ? 2LL * p.P * WF_TILE : static_cast<int64_t>(p.P) * WF_TILE;
+  if (N <= 0 || N % q) return fail(ctx, WF_ERR_CONFIG, "N must be a positive multiple of " + std::to_string(q));
+  if (N / p.P > (1LL << 30) / 2) return fail(ctx, WF_ERR_CONFIG, "N/P too large");
+  g->P = p.P;
+  g->C = p.C;
+  g->T = p.T;
+  g->R = p.R;
+  g->W = p.W;
+  g->paper = p.paper;
+  g->causal = causal != 0;
+  g->N = N;
+  g->n = static_cast<int>(N / p.P);
+  g->c = causal ? static_cast<int>(N / (2 * p.P)) : g->n;
+  g->h = heads;
+  g->d = head_dim;
+  g->E = static_cast<int64_t>(heads) * head_dim;
+  g->Bk = p.paper ? p.C * g->n : p.W * g->n;
+  if (p.C > WF_MAX_PARTS || (!p.paper && p.T > WF_MAX_PARTS) || 2 * std::max(p.C, p.W) > WF_MAX_CHUNKS)
+    return fail(ctx, WF_ERR_CONFIG, "P/C too large for this build");
+  return WF_OK;
+}
+
+// Chunk position table of a list of units (zigzag: two chunks per unit).
+PosTable units_table(const Geo& g, int u0, int count) {
+  PosTable t;
+  std::memset(&t, 0, sizeof(t));
+  t.chunk = g.c;
+  int k = 0;
+  for (int u = u0; u < u0 + count; ++u) {
+    if (g.causal) {
+      t.start[k++] = u * g.c;
+      t.start[k++] = (2 * g.P - 1 - u) * g.c;
+    } else {
+      t.start[k++] = u * g.n;
+    }
+  }
+  t.nchunks = k;
+  return t;
+}
+
+// ------------------------------------------------------------------ workspace
+wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
+  if (ctx->dry) {
+    ctx->rb.assign(ctx->plan.P, RankBufs{});
+    return WF_OK;
+  }
+  const int64_t key[4] = {g.N, g.h, g.d, g.causal};
+  if (ctx->ws && std::equal(key, key + 4, ctx->ws_key)) return WF_OK;
+  if (ctx->ws) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaFree(ctx->ws));
+    ctx->ws = nullptr;
+  }
+  const int nranks = ctx->emulated ? g.P : 1;
+  const int64_t C = g.C, n = g.n, E = g.E, h = g.h, Bk = g.Bk;
+  const int64_t team = C * n * E;  // elements of a team tensor
+  // carve plan (bytes), per rank
+  std::vector<std::pair<void**, int64_t>> items;
+  std::vector<RankBufs> rb(nranks);
+  for (auto& b : rb) {
+    auto add = [&](auto** p, int64_t bytes) { items.push_back({reinterpret_cast<void**>(p), bytes}); };
+    if (C > 1) {
+      add(&b.qt, team * 2);
+      add(&b.t_do, team * 2);
+      add(&b.t_lse, C * h * n * 4);
+      add(&b.t_dsum, C * h * n * 4);
+      add(&b.o_part, team * 2);
+      add(&b.rs_o, team * 2);
+      add(&b.rs_lse, C * h * n * 4);
+      add(&b.rsq, team * 4);
+      if (g.paper) {
+        add(&b.kt, team * 2);
+        add(&b.vt, team * 2);
+        add(&b.rsk, team * 4);
+        add(&b.rsv, team * 4);
+      }
+    }
+    for (int s = 0; s < 2; ++s) {
+      add(&b.rk[s], Bk * E * 2);
+      add(&b.rv[s], Bk * E * 2);
+    }
+    add(&b.o_state, team * 4);
+    add(&b.lse_state, C * h * n * 4);
+    add(&b.dsum, h * n * 4);
+    for (int s = 0; s < 2; ++s) {
+      add(&b.pdq[s], team * 4);
+      if (g.R > 1) {
+        add(&b.pq[s], team * 2);
+        add(&b.pdo[s], team * 2);
+        add(&b.plse[s], C * h * n * 4);
+        add(&b.pdsum[s], C * h * n * 4);
+      }
+    }
+    if (g.R > 1) add(&b.home_dq, team * 4);
+    add(&b.dk_acc, Bk * E * 4);
+    add(&b.dv_acc, Bk * E * 4);
+    if (g.paper) {
+      if (C > 1) {
+        add(&b.rev_k, team * 4);
+        add(&b.rev_v, team * 4);
+      }
+    } else {
+      add(&b.rev_k, static_cast<int64_t>(g.T) * n * E * 4);
+      add(&b.rev_v, static_cast<int64_t>(g.T) * n * E * 4);
+    }
+  }
+  size_t total = 0;
+  for (auto& it : items) total += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
+  void* base = nullptr;
+  CK(cudaMalloc(&base, total));
+  size_t off = 0;
+  for (auto& it : items) {
+    *it.first = static_cast<char*>(base) + off;
+    off += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
+  }
+  ctx->ws = base;
+  ctx->ws_bytes = total;
+  std::copy(key, key + 4, ctx->ws_key);
+  ctx->rb = rb;
+  return WF_OK;
+}
+
+RankBufs& B(wf_ctx* ctx, int r) { return ctx->rb[ctx->emulated || ctx->dry ? r : 0]; }
+
+// ------------------------------------------------------------------ transport
+wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& trace, cudaStream_t st) {
+  for (const Xfer& x : xs) {
+    if (x.src == x.dst || !recorded(ctx, x.src)) continue;
+    int64_t bytes = 0;
+    for (const Seg& s : x.segs) bytes += s.bytes;
+    trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
+  }
+  if (ctx->dry) return WF_OK;
+  if (ctx->emulated) {
+    for (const Xfer& x : xs)
+      for (const Seg& s : x.segs)
+        if (s.bytes && s.src != s.dst) CK(cudaMemcpyAsync(s.dst, s.src, s.bytes, cudaMemcpyDeviceToDevice, st));
+    return WF_OK;
+  }
+  const int me = ctx->rank;
+  bool any = false;
+  for (const Xfer& x : xs) any = any || ((x.src == me) != (x.dst == me));
+  if (any) NCK(ncclGroupStart());
+  for (const Xfer& x : xs) {
+    for (const Seg& s : x.segs) {
+      if (!s.bytes) continue;
+      if (x.src == me && x.dst == me) {
+        if (s.src != s.dst) CK(cudaMemcpyAsync(s.dst, s.src, s.bytes, cudaMemcpyDeviceToDevice, st));
+      } else if (x.src == me) {
+        NCK(ncclSend(s.src, static_cast<size_t>(s.bytes), ncclInt8, x.dst, ctx->comm, st));
+      } else if (x.dst == me) {
+        NCK(ncclRecv(s.dst, static_cast<size_t>(s.bytes), ncclInt8, x.src, ctx->comm, st));
+      }
+    }
+  }
+  if (any) NCK(ncclGroupEnd());
+  return WF_OK;
+}
+
+// pointer helpers that are null for non-local ranks
+template <typename T>
+T* at(T* base, int64_t off) {
+  return base ? base + off : nullptr;
+}
+
+wf_status kcheck(wf_ctx* ctx, cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(ctx, WF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  ++ctx->launches;
+  return WF_OK;
+}
+
+// ------------------------------------------------------------------ forward
+wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const bf16* V, bf16* O, float* LSE,
+                  cudaStream_t st) {
+  const Plan& pl = ctx->plan;
+  const int P = g.P, C = g.C, R = g.R;
+  const int64_t n = g.n, E = g.E, h = g.h;
+  auto Qin = [&](int r) { return local(ctx, r) ? Q + (ctx->emulated ? r * n * E : 0) : nullptr; };
+  auto Kin = [&](int r) { return local(ctx, r) ? K + (ctx->emulated ? r * n * E : 0) : nullptr; };
+  auto Vin = [&](int r) { return local(ctx, r) ? V + (ctx->emulated ? r * n * E : 0) : nullptr; };
+  auto Oout = [&](int r) { return local(ctx, r) ? O + (ctx->emulated ? r * n * E : 0) : nullptr; };
+  auto Lout = [&](int r) { return local(ctx, r) ? LSE + (ctx->emulated ? r * n * h : 0) : nullptr; };
+  auto lp = [&](int r, auto* p) { return local(ctx, r) ? p : decltype(p)(nullptr); };
+  auto& tr = ctx->trace_fwd;
+  tr.clear();
+
+  // Team tensors (C = 1: the caller's shard itself).
+  auto qteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).qt) : Qin(r); };
+  auto kteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).kt) : Kin(r); };
+  auto vteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).vt) : Vin(r); };
+
+  // Alg. 1 l.1: team all-gather (member-major).
+  if (C > 1) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int t = r / C, j = r - t * C;
+      for (int p = t * C; p < t * C + C; ++p) {
+        Xfer x{0, WF_KIND_AG_Q, -1, r, p, r, {}};
+        x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+        xs.push_back(x);
+        if (g.paper) {
+          Xfer y{0, WF_KIND_AG_KV, -1, r, p, r, {}};
+          y.segs.push_back({Kin(r), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
+          y.segs.push_back({Vin(r), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
+          xs.push_back(y);
+        }
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+  }
+
+  // Per rank: pointers of the K/V block in ring slot 0/1.
+  std::vector<const bf16*> ck0(P, nullptr), cv0(P, nullptr);
+  if (g.paper) {
+    // Alg. 1 l.2: initial shuffle to init_send (a self "send" keeps the block in place).
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int dst = pl.send[r];
+      if (dst == r) continue;
+      Xfer x{0, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
+      x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), static_cast<int64_t>(C) * n * E * 2});
+      x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), static_cast<int64_t>(C) * n * E * 2});
+      xs.push_back(x);
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int r = 0; r < P; ++r) {
+      if (pl.send[r] == r) {  // recv[r] == r too
+        ck0[r] = kteam(r);
+        cv0[r] = vteam(r);
+      } else {
+        ck0[r] = lp(r, B(ctx, r).rk[0]);
+        cv0[r] = lp(r, B(ctx, r).rv[0]);
+      }
+    }
+  } else {
+    // extension: member a pulls K/V slice a straight from the unit owners.
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int a = r % C;
+      for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
+        const int64_t off = static_cast<int64_t>(u - a * g.W) * n * E;
+        Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+        x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
+        x.segs.push_back({Vin(u), at(lp(r, B(ctx, r).rv[0]), off), n * E * 2});
+        xs.push_back(x);
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int r = 0; r < P; ++r) {
+      ck0[r] = lp(r, B(ctx, r).rk[0]);
+      cv0[r] = lp(r, B(ctx, r).rv[0]);
+    }
+  }
+
+  // Alg. 1 l.5-10: R ring steps, K/V double buffered; the transfer of block s+1
+  // (comm stream) is posted before the block kernel of step s.
+  const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
+  auto slot_k = [&](int r, int s) -> const bf16* { return s == 0 ? ck0[r] : lp(r, B(ctx, r).rk[s & 1]); };
+  auto slot_v = [&](int r, int s) -> const bf16* { return s == 0 ? cv0[r] : lp(r, B(ctx, r).rv[s & 1]); };
+  auto compute = [&](int r, int s) -> wf_status {
+    RankBufs& b = B(ctx, r);
+    FwdArgs a{};
+    a.nq = C * g.n;
+    a.nk = g.Bk;
+    a.heads = g.h;
+    a.causal = g.causal;
+    a.qpos = units_table(g, (r / C) * C, C);
+    a.kpos = g.paper ? units_table(g, pl.block_at(r, s) * C, C) : units_table(g, (r % C) * g.W, g.W);
+    a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(g.d));
+    a.o_in = s > 0 ? b.o_state : nullptr;
+    a.lse_in = s > 0 ? b.lse_state : nullptr;
+    a.lse_blk = g.n;
+    if (s < R - 1) {  // intermediate step: fp32 (O, lse) state, merged in place next step
+      a.o_out_f32 = b.o_state;
+      a.lse_out = b.lse_state;
+    } else if (C == 1) {  // final output
+      a.o_out_bf16 = Oout(r);
+      a.lse_out = Lout(r);
+    } else {  // this member's partial for the team rows
+      a.o_out_bf16 = b.o_part;
+      a.lse_out = b.lse_state;
+    }
+    if (ctx->dry) return WF_OK;
+    CUtensorMap tq, tk, tv;
+    if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
+        !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
+      return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+    return kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
+  };
+  if (overlap) CK(cudaEventRecord(ctx->ev_a, st));  // slot 0 ready
+  for (int s = 0; s < R; ++s) {
+    std::vector<Xfer> xs;
+    if (s < R - 1) {
+      for (int r = 0; r < P; ++r) {
+        const int dst = pl.next[r];
+        Xfer x{0, WF_KIND_RING_KV, s, r, dst, g.paper ? pl.block_at(r, s) : r, {}};
+        x.segs.push_back({slot_k(r, s), lp(dst, B(ctx, dst).rk[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
+        x.segs.push_back({slot_v(r, s), lp(dst, B(ctx, dst).rv[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
+        xs.push_back(x);
+      }
+      if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+        WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
+        CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+      }
+    }
+    for (int r = 0; r < P; ++r)
+      if (local(ctx, r)) WCK(compute(r, s));
+    if (s < R - 1) {
+      if (overlap) {
+        CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
+        CK(cudaEventRecord(ctx->ev_a, st));
+      } else {
+        WCK(run_phase(ctx, xs, tr, st));
+      }
+    }
+  }
+
+  // Alg. 1 l.11: ReduceScatter_combine -- partial rows to their owner, LSE-merge there.
+  if (C > 1) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int t = r / C, j = r - t * C;
+      for (int p = t * C; p < t * C + C; ++p) {
+        if (p == r) continue;
+        const int jp = p - t * C;
+        Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}};
+        x.segs.push_back({at(lp(r, B(ctx, r).o_part), jp * n * E), at(lp(p, B(ctx, p).rs_o), j * n * E), n * E * 2});
+        xs.push_back(x);
+        Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}};
+        y.segs.push_back({at(lp(r, B(ctx, r).lse_state), jp * h * n), at(lp(p, B(ctx, p).rs_lse), j * h * n), h * n * 4});
+        xs.push_back(y);
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int r = 0; r < P; ++r) {
+      if (!local(ctx, r)) continue;
+      RankBufs& b = B(ctx, r);
+      const int j = r % C;
+      MergeArgs m{};
+      m.rows = g.n;
+      m.heads = g.h;
+      m.D = g.d;
+      m.nparts = C;
+      for (int i = 0; i < C; ++i) {
+        m.o[i] = i == j ? b.o_part + i * n * E : b.rs_o + i * n * E;
+        m.lse[i] = i == j ? b.lse_state + i * h * n : b.rs_lse + i * h * n;
+        m.lse_stride[i] = n;
+      }
+      m.out = Oout(r);
+      m.lse_out = Lout(r);
+      if (!ctx->dry) WCK(kcheck(ctx, launch_merge(m, st), "merge"));
+    }
+  }
+  return WF_OK;
+}
+
+// ------------------------------------------------------------------ backward
+wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, const bf16* K, const bf16* V,
+                   const bf16* O, const float* LSE, bf16* dQ, bf16* dK, bf16* dV, cudaStream_t st) {
+  const Plan& pl = ctx->plan;
+  const int P = g.P, C = g.C, R = g.R, T = g.T;
+  const int64_t n = g.n, E = g.E, h = g.h, team = static_cast<int64_t>(C) * n * E;
+  auto off = [&](int r, int64_t per) { return ctx->emulated ? r * per : 0; };
+  auto L = [&](int r, auto* p, int64_t per) { return local(ctx, r) ? p + off(r, per) : decltype(p)(nullptr); };
+  auto lp = [&](int r, auto* p) { return local(ctx, r) ? p : decltype(p)(nullptr); };
+  auto& tr = ctx->trace_bwd;
+  tr.clear();
+
+  // D = rowsum(dO o O) on own rows (reading c12).
+  for (int r = 0; r < P; ++r) {
+    if (!local(ctx, r) || ctx->dry) continue;
+    WCK(kcheck(ctx, launch_dsum(L(r, dO, n * E), L(r, O, n * E), B(ctx, r).dsum, g.n, g.h, g.d, st), "dsum"));
+  }
+  auto qteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).qt) : L(r, Q, n * E); };
+  auto doteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).t_do) : L(r, dO, n * E); };
+  auto lseteam = [&](int r) -> const float* { return C > 1 ? lp(r, B(ctx, r).t_lse) : L(r, LSE, n * h); };
+  auto dsteam = [&](int r) -> const float* { return C > 1 ? lp(r, B(ctx, r).t_dsum) : lp(r, B(ctx, r).dsum); };
+  auto kteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).kt) : L(r, K, n * E); };
+  auto vteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).vt) : L(r, V, n * E); };
+
+  // team gathers: Q + dO, LSE + D, and (paper regime) K + V
+  if (C > 1) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int t = r / C, j = r - t * C;
+      for (int p = t * C; p < t * C + C; ++p) {
+        Xfer x{1, WF_KIND_AG_QDO, -1, r, p, r, {}};
+        x.segs.push_back({L(r, Q, n * E), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+        x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
+        xs.push_back(x);
+        Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
+        y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
+        y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
+        xs.push_back(y);
+        if (g.paper) {
+          Xfer z{1, WF_KIND_AG_KV, -1, r, p, r, {}};
+          z.segs.push_back({L(r, K, n * E), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
+          z.segs.push_back({L(r, V, n * E), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
+          xs.push_back(z);
+        }
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+  }
+
+  // stationary K/V block: the init-shuffle block (paper) or the slice (extension)
+  std::vector<const bf16*> sk(P, nullptr), sv(P, nullptr);
+  {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      if (g.paper) {
+        const int dst = pl.send[r];
+        if (dst == r) continue;
+        Xfer x{1, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
+        x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), team * 2});
+        x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), team * 2});
+        xs.push_back(x);
+      } else {
+        const int a = r % C;
+        for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
+          const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
+          Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+          x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
+          x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
+          xs.push_back(x);
+        }
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int r = 0; r < P; ++r) {
+      const bool self = g.paper && pl.send[r] == r;
+      sk[r] = self ? kteam(r) : lp(r, B(ctx, r).rk[0]);
+      sv[r] = self ? vteam(r) : lp(r, B(ctx, r).rv[0]);
+    }
+  }
+
+  // package slots: step 0 = own team (aliases); later steps in the receive buffers
+  auto pq = [&](int r, int s) -> const bf16* { return s == 0 ? qteam(r) : lp(r, B(ctx, r).pq[s & 1]); };
+  auto pdo = [&](int r, int s) -> const bf16* { return s == 0 ? doteam(r) : lp(r, B(ctx, r).pdo[s & 1]); };
+  auto plse = [&](int r, int s) -> const float* { return s == 0 ? lseteam(r) : lp(r, B(ctx, r).plse[s & 1]); };
+  auto pds = [&](int r, int s) -> const float* { return s == 0 ? dsteam(r) : lp(r, B(ctx, r).pdsum[s & 1]); };
+  auto pdq = [&](int r, int s) -> float* { return lp(r, B(ctx, r).pdq[s & 1]); };
+  std::vector<int> pkg_team(P);
+  for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
+  for (int r = 0; r < P; ++r)
+    if (local(ctx, r) && !ctx->dry) CK(cudaMemsetAsync(pdq(r, 0), 0, team * 4, st));
+
+  const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
+  if (overlap) CK(cudaEventRecord(ctx->ev_a, st));
+  for (int s = 0; s < R; ++s) {
+    std::vector<Xfer> pk, dq;
+    if (s < R - 1) {
+      for (int r = 0; r < P; ++r) {
+        const int dst = pl.next[r];
+        const int s1 = (s + 1) & 1;
+        Xfer x{1, WF_KIND_RING_QPKG, s, r, dst, pkg_team[r], {}};
+        x.segs.push_back({pq(r, s), lp(dst, B(ctx, dst).pq[s1]), team * 2});
+        x.segs.push_back({pdo(r, s), lp(dst, B(ctx, dst).pdo[s1]), team * 2});
+        x.segs.push_back({plse(r, s), lp(dst, B(ctx, dst).plse[s1]), C * h * n * 4});
+        x.segs.push_back({pds(r, s), lp(dst, B(ctx, dst).pdsum[s1]), C * h * n * 4});
+        pk.push_back(x);
+        Xfer y{1, WF_KIND_RING_DQ, s, r, dst, pkg_team[r], {}};
+        y.segs.push_back({pdq(r, s), lp(dst, B(ctx, dst).pdq[s1]), team * 4});
+        dq.push_back(y);
+      }
+      if (overlap) {  // the package does not depend on step s: post it first
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+        WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
+      }
+    }
+    for (int r = 0; r < P; ++r) {
+      if (!local(ctx, r)) continue;
+      RankBufs& b = B(ctx, r);
+      BwdArgs a{};
+      a.nq = C * g.n;
+      a.nk = g.Bk;
+      a.heads = g.h;
+      a.causal = g.causal;
+      a.qpos = units_table(g, pkg_team[r] * C, C);
+      a.kpos = g.paper ? units_table(g, (pl.recv[r] / C) * C, C) : units_table(g, (r % C) * g.W, g.W);
+      a.scale = 1.f / std::sqrt(static_cast<float>(g.d));
+      a.scale_log2 = 1.4426950408889634f * a.scale;
+      a.lse = plse(r, s);
+      a.dsum = pds(r, s);
+      a.stat_blk = g.n;
+      a.dq_acc = pdq(r, s);
+      a.dk_acc = b.dk_acc;
+      a.dv_acc = b.dv_acc;
+      a.dkv_accumulate = s > 0;
+      if (ctx->dry) continue;
+      CUtensorMap tq, tk, tv, tdo;
+      if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
+          !make_tmap_rows(&tv, sv[r], a.nk, g.h, g.d) || !make_tmap_rows(&tdo, pdo(r, s), a.nq, g.h, g.d))
+        return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+      WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, a, g.d, st), "block_bwd"));
+    }
+    if (s < R - 1) {
+      if (overlap) {
+        // dQ depends on step s: after it; the receiver's next step waits for both
+        CK(cudaEventRecord(ctx->ev_b, st));
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+        WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
+        CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+        CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
+        CK(cudaEventRecord(ctx->ev_a, st));
+      } else {
+        WCK(run_phase(ctx, pk, tr, st));
+        WCK(run_phase(ctx, dq, tr, st));
+      }
+      std::vector<int> nt(P);
+      for (int r = 0; r < P; ++r) nt[pl.next[r]] = pkg_team[r];
+      pkg_team = nt;
+    }
+  }
+
+  // return hop: dQ back to its home
+  std::vector<float*> home(P, nullptr);
+  if (R > 1) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int dst = pl.next[r];
+      Xfer x{1, WF_KIND_RET_DQ, R - 1, r, dst, pkg_team[r], {}};
+      x.segs.push_back({pdq(r, R - 1), lp(dst, B(ctx, dst).home_dq), team * 4});
+      xs.push_back(x);
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int r = 0; r < P; ++r) home[r] = lp(r, B(ctx, r).home_dq);
+  } else {
+    for (int r = 0; r < P; ++r) home[r] = pdq(r, 0);
+  }
+
+  // dK/dV: reverse shuffle (paper) or straight to the unit owners (extension)
+  std::vector<std::vector<const float*>> kparts(P), vparts(P);
+  if (g.paper) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int dst = pl.recv[r];
+      if (dst == r) continue;
+      Xfer x{1, WF_KIND_REV_DKV, R, r, dst, pl.recv[r] / C, {}};
+      x.segs.push_back({lp(r, B(ctx, r).dk_acc), lp(dst, B(ctx, dst).rev_k), team * 4});
+      x.segs.push_back({lp(r, B(ctx, r).dv_acc), lp(dst, B(ctx, dst).rev_v), team * 4});
+      xs.push_back(x);
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    // replica partial of my team's block: received from init_send[r] (or my own when self)
+    std::vector<const float*> rk(P), rv(P);
+    for (int r = 0; r < P; ++r) {
+      const bool self = pl.send[r] == r;
+      rk[r] = self ? lp(r, B(ctx, r).dk_acc) : lp(r, B(ctx, r).rev_k);
+      rv[r] = self ? lp(r, B(ctx, r).dv_acc) : lp(r, B(ctx, r).rev_v);
+    }
+    if (C > 1) {
+      std::vector<Xfer> ys;
+      for (int r = 0; r < P; ++r) {
+        const int t = r / C, j = r - t * C;
+        for (int p = t * C; p < t * C + C; ++p) {
+          if (p == r) continue;
+          const int jp = p - t * C;
+          Xfer x{1, WF_KIND_RS_DKV, R, r, p, p, {}};
+          x.segs.push_back({at(rk[r], jp * n * E), at(lp(p, B(ctx, p).rsk), j * n * E), n * E * 4});
+          x.segs.push_back({at(rv[r], jp * n * E), at(lp(p, B(ctx, p).rsv), j * n * E), n * E * 4});
+          ys.push_back(x);
+        }
+      }
+      WCK(run_phase(ctx, ys, tr, st));
+    }
+    for (int r = 0; r < P; ++r) {
+      const int j = r % C;
+      for (int i = 0; i < C; ++i) {
+        kparts[r].push_back(i == j ? at(rk[r], i * n * E) : at(lp(r, B(ctx, r).rsk), i * n * E));
+        vparts[r].push_back(i == j ? at(rv[r], i * n * E) : at(lp(r, B(ctx, r).rsv), i * n * E));
+      }
+    }
+  } else {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int a = r % C;
+      for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
+        const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
+        const int slot = r / C;
+        Xfer x{1, WF_KIND_REV_DKV, R, r, u, u, {}};
+        if (u == r) continue;
+        x.segs.push_back({at(lp(r, B(ctx, r).dk_acc), o), at(lp(u, B(ctx, u).rev_k), slot * n * E), n * E * 4});
+        x.segs.push_back({at(lp(r, B(ctx, r).dv_acc), o), at(lp(u, B(ctx, u).rev_v), slot * n * E), n * E * 4});
+        xs.push_back(x);
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+    for (int u = 0; u < P; ++u) {
+      const int a = u / g.W;
+      for (int t = 0; t < T; ++t) {
+        const int r = t * C + a;
+        const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
+        kparts[u].push_back(r == u ? at(lp(u, B(ctx, u).dk_acc), o) : at(lp(u, B(ctx, u).rev_k), t * n * E));
+        vparts[u].push_back(r == u ? at(lp(u, B(ctx, u).dv_acc), o) : at(lp(u, B(ctx, u).rev_v), t * n * E));
+      }
+    }
+  }
+
+  // dQ team reduce-scatter
+  std::vector<std::vector<const float*>> qparts(P);
+  if (C > 1) {
+    std::vector<Xfer> xs;
+    for (int r = 0; r < P; ++r) {
+      const int t = r / C, j = r - t * C;
+      for (int p = t * C; p < t * C + C; ++p) {
+        if (p == r) continue;
+        const int jp = p - t * C;
+        Xfer x{1, WF_KIND_RS_DQ, R, r, p, p, {}};
+        x.segs.push_back({at(home[r], jp * n * E), at(lp(p, B(ctx, p).rsq), j * n * E), n * E * 4});
+        xs.push_back(x);
+      }
+    }
+    WCK(run_phase(ctx, xs, tr, st));
+  }
+  for (int r = 0; r < P; ++r) {
+    const int j = r % C;
+    for (int i = 0; i < C; ++i)
+      qparts[r].push_back(i == j ? at(home[r], i * n * E) : at(lp(r, B(ctx, r).rsq), i * n * E));
+  }
+  if (ctx->dry) return WF_OK;
+  for (int r = 0; r < P; ++r) {
+    if (!local(ctx, r)) continue;
+    const std::vector<const float*>* parts[3] = {&qparts[r], &kparts[r], &vparts[r]};
+    bf16* outs[3] = {L(r, dQ, n * E), L(r, dK, n * E), L(r, dV, n * E)};
+    for (int i = 0; i < 3; ++i) {
+      SumArgs s{};
+      s.n = n * E;
+      s.nparts = static_cast<int>(parts[i]->size());
+      for (int k = 0; k < s.nparts; ++k) s.parts[k] = (*parts[i])[k];
+      s.out = outs[i];
+      WCK(kcheck(ctx, launch_sum(s, st), "sum"));
+    }
+  }
+  return WF_OK;
+}
+
+wf_status new_ctx(int P, int C, wf_ctx** out, wf_ctx** tmp) {
+  auto* ctx = new wf_ctx();
+  *tmp = ctx;
+  std::string err;
+  if (!build_plan(P, C, &ctx->plan, &err)) {
+    delete ctx;
+    *tmp = nullptr;
+    return fail(nullptr, WF_ERR_CONFIG, err);
+  }
+  *out = ctx;
+  return WF_OK;
+}
+
+wf_status make_streams(wf_ctx* ctx) {
+  CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+  return WF_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+wf_status wf_get_uid(wf_uid* out) {
+  if (!out) return fail(nullptr, WF_ERR_ARG, "wf_get_uid: null");
+  static_assert(sizeof(ncclUniqueId) <= sizeof(wf_uid), "uid size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, WF_ERR_COMM, ncclGetErrorString(r));
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->bytes, &id, sizeof(id));
+  return WF_OK;
+}
+
+wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, wf_ctx** out) {
+  if (!out) return fail(nullptr, WF_ERR_ARG, "wf_init: null out");
+  if (topo != WF_TOPO_COLLECT_INTRA && topo != WF_TOPO_P2P_INTRA) return fail(nullptr, WF_ERR_CONFIG, "bad topology");
+  if (rank < 0 || rank >= P) return fail(nullptr, WF_ERR_CONFIG, "rank out of range");
+  wf_ctx* ctx = nullptr;
+  wf_ctx* tmp = nullptr;
+  WCK(new_ctx(P, C, &ctx, &tmp));
+  ctx->rank = rank;
+  wf_status s = make_streams(ctx);
+  if (s != WF_OK) {
+    g_ctxless_err = ctx->err;
+    wf_finalize(ctx);
+    return s;
+  }
+  if (P > 1) {
+    if (!uid) {
+      wf_finalize(ctx);
+      return fail(nullptr, WF_ERR_ARG, "wf_init: uid required when P > 1");
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, uid->bytes, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, P, id, rank);
+    if (r != ncclSuccess) {
+      wf_finalize(ctx);
+      return fail(nullptr, WF_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+  }
+  *out = ctx;
+  return WF_OK;
+}
+
+wf_status wf_init_emulated(int P, int C, wf_ctx** out) {
+  if (!out) return fail(nullptr, WF_ERR_ARG, "wf_init_emulated: null out");
+  wf_ctx* ctx = nullptr;
+  wf_ctx* tmp = nullptr;
+  WCK(new_ctx(P, C, &ctx, &tmp));
+  ctx->emulated = true;
+  wf_status s = make_streams(ctx);
+  if (s != WF_OK) {
+    g_ctxless_err = ctx->err;
+    wf_finalize(ctx);
+    return s;
+  }
+  *out = ctx;
+  return WF_OK;
+}
+
+wf_status wf_attn_fwd(wf_ctx* ctx, const void* Q, const void* K, const void* V, int64_t N, int heads, int head_dim,
+                      int causal, void* O, float* LSE, void* stream) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  if (!Q || !K || !V || !O || !LSE) return fail(ctx, WF_ERR_ARG, "wf_attn_fwd: null pointer");
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
+    return fail(ctx, WF_ERR_ARG, "wf_attn_fwd: pointers must be 16-byte aligned");
+  Geo g;
+  WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
+  WCK(ensure_ws(ctx, g));
+  return forward(ctx, g, static_cast<const bf16*>(Q), static_cast<const bf16*>(K), static_cast<const bf16*>(V),
+                 static_cast<bf16*>(O), LSE, static_cast<cudaStream_t>(stream));
+}
+
+wf_status wf_attn_bwd(wf_ctx* ctx, const void* dO, const void* Q, const void* K, const void* V, const void* O,
+                      const float* LSE, int64_t N, int heads, int head_dim, int causal, void* dQ, void* dK, void* dV,
+                      void* stream) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  if (!dO || !Q || !K || !V || !O || !LSE || !dQ || !dK || !dV) return fail(ctx, WF_ERR_ARG, "wf_attn_bwd: null pointer");
+  for (const void* p : {dO, Q, K, V, O, static_cast<const void*>(LSE), static_cast<const void*>(dQ),
+                        static_cast<const void*>(dK), static_cast<const void*>(dV)})
+    if (!aligned16(p)) return fail(ctx, WF_ERR_ARG, "wf_attn_bwd: pointers must be 16-byte aligned");
+  Geo g;
+  WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
+  WCK(ensure_ws(ctx, g));
+  return backward(ctx, g, static_cast<const bf16*>(dO), static_cast<const bf16*>(Q), static_cast<const bf16*>(K),
+                  static_cast<const bf16*>(V), static_cast<const bf16*>(O), LSE, static_cast<bf16*>(dQ),
+                  static_cast<bf16*>(dK), static_cast<bf16*>(dV), static_cast<cudaStream_t>(stream));
+}
+
+static wf_status copy_trace(const std::vector<wf_event>& a, const std::vector<wf_event>& b, wf_event* buf, size_t cap,
+                            size_t* n_out) {
+  const size_t n = a.size() + b.size();
+  if (n_out) *n_out = n;
+  if (buf) {
+    size_t k = 0;
+    for (const auto& e : a)
+      if (k < cap) buf[k++] = e;
+    for (const auto& e : b)
+      if (k < cap) buf[k++] = e;
+  }
+  return WF_OK;
+}
+
+wf_status wf_get_trace(wf_ctx* ctx, wf_event* buf, size_t cap, size_t* n_out) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  return copy_trace(ctx->trace_fwd, ctx->trace_bwd, buf, cap, n_out);
+}
+
+wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,
+                        size_t* n_out) {
+  wf_ctx* ctx = nullptr;
+  wf_ctx* tmp = nullptr;
+  WCK(new_ctx(P, C, &ctx, &tmp));
+  std::unique_ptr<wf_ctx> hold(ctx);
+  ctx->dry = true;
+  ctx->dry_rank = rank;
+  Geo g;
+  // full-mask geometry (the trace is mask independent)
+  wf_status s = check_shape(ctx, N, heads, head_dim, 0, &g);
+  if (s != WF_OK) return fail(nullptr, s, ctx->err);
+  ensure_ws(ctx, g);
+  s = forward(ctx, g, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (s == WF_OK) s = backward(ctx, g, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (s != WF_OK) return fail(nullptr, s, ctx->err);
+  return copy_trace(ctx->trace_fwd, ctx->trace_bwd, buf, cap, n_out);
+}
+
+wf_status wf_plan(int P, int C, int rank, int32_t out[6]) {
+  Plan p;
+  std::string err;
+  if (!build_plan(P, C, &p, &err)) return fail(nullptr, WF_ERR_CONFIG, err);
+  if (rank < 0 || rank >= P || !out) return fail(nullptr, WF_ERR_ARG, "wf_plan: bad rank/out");
+  out[0] = p.send[rank];
+  out[1] = p.recv[rank];
+  out[2] = p.next[rank];
+  out[3] = p.last[rank];
+  out[4] = p.R;
+  out[5] = p.paper ? 0 : 1;
+  return WF_OK;
+}
+
+wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges[4]) {
+  if (P < 1 || rank < 0 || rank >= P || !ranges) return fail(nullptr, WF_ERR_ARG, "wf_shard_ranges: bad args");
+  if (causal) {
+    if (N % (2 * P)) return fail(nullptr, WF_ERR_CONFIG, "zigzag needs 2P | N");
+    const int64_t c = N / (2 * P);
+    ranges[0] = rank * c;
+    ranges[1] = (rank + 1) * c;
+    ranges[2] = (2LL * P - 1 - rank) * c;
+    ranges[3] = (2LL * P - rank) * c;
+  } else {
+    if (N % P) return fail(nullptr, WF_ERR_CONFIG, "naive split needs P | N");
+    const int64_t n = N / P;
+    ranges[0] = rank * n;
+    ranges[1] = (rank + 1) * n;
+    ranges[2] = ranges[3] = ranges[1];
+  }
+  return WF_OK;
+}
+
+int64_t wf_kernel_launches(const wf_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* wf_last_error(const wf_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  if (!g_ctxless_err.empty()) return g_ctxless_err.c_str();
+  return wf_static_error();
+}
+
+wf_status wf_finalize(wf_ctx* ctx) {
+  if (!ctx) return WF_OK;
+  if (ctx->ws) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->ws);
+  }
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  delete ctx;
+  return WF_OK;
+}
+
+}  // extern "C"

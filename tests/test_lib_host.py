@@ -1,0 +1,94 @@
+"""Host-side tests of libwf.so (no GPU needed): the C ABI loads and exports every
+symbol include/wf.h declares; the library's plan equals Alg. 2/3 as the oracle
+transcribes it; its CommTrace (wf_plan_trace) equals the oracle's literal schedule
+simulation record for record (bit-exact bookkeeping)."""
+import os
+import re
+from collections import Counter
+
+import pytest
+
+from oracle.schedule import simulate_backward, simulate_forward
+from oracle.sharding import unit_positions
+from oracle.topology import ConfigError, build_plan, regime
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def wf():
+    from paper_2407_00611_b200 import build
+    build.build()
+    import paper_2407_00611_b200 as m
+    return m
+
+
+def test_exports_every_declared_symbol(wf):
+    from paper_2407_00611_b200._lib import EXPORTED, lib
+    hdr = open(os.path.join(ROOT, "include", "wf.h")).read()
+    declared = set(re.findall(r"^\s*(?:wf_status|int64_t|const char\*)\s+(wf_\w+)\s*\(", hdr, re.M))
+    assert declared, "no declarations parsed"
+    L = lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert declared == set(EXPORTED)
+
+
+@pytest.mark.parametrize("P,C", [(P, C) for P in range(1, 17) for C in range(1, P + 1)])
+def test_plan_matches_oracle(wf, P, C):
+    try:
+        o = build_plan(P, C)
+    except ConfigError:
+        with pytest.raises(wf.WFError):
+            wf.plan(P, C, 0)
+        return
+    for r in range(P):
+        p = wf.plan(P, C, r)
+        assert (p["send"], p["recv"], p["next"], p["last"], p["R"], p["regime"]) == \
+            (o["send"][r], o["recv"][r], o["next"][r], o["last"][r], o["R"], o["regime"])
+
+
+def _oracle_trace(P, C, N, h, d):
+    _, _, ev_f, _ = simulate_forward(N, None, None, P, C, False, compute=False, heads=h, head_dim=d)
+    _, _, _, ev_b = simulate_backward(N, None, None, None, None, None, P, C, False, compute=False, heads=h, head_dim=d)
+    return Counter((e.pas, e.kind, e.step, e.src, e.dst, e.block, e.nbytes) for e in ev_f + ev_b)
+
+
+CFGS = [(P, C) for P in (1, 2, 3, 4, 6, 8, 12, 16) for C in (1, 2, 3, 4, 8)
+        if C <= P and P % C == 0 and (C * C > P or P % (C * C) == 0) and C <= 8 and P // C <= 8 or (P, C) == (16, 4)]
+
+
+@pytest.mark.parametrize("P,C", CFGS)
+def test_plan_trace_equals_oracle(wf, P, C):
+    N, h, d = 256 * P, 2, 64
+    lib_tr = Counter(wf.plan_trace(P, C, N, h, d))
+    assert lib_tr == _oracle_trace(P, C, N, h, d)
+
+
+def test_plan_trace_per_rank_partition(wf):
+    P, C, N = 8, 2, 2048
+    full = Counter(wf.plan_trace(P, C, N, 2, 64))
+    parts = Counter()
+    for r in range(P):
+        tr = wf.plan_trace(P, C, N, 2, 64, rank=r)
+        assert all(e[3] == r for e in tr)
+        parts.update(tr)
+    assert parts == full
+
+
+def test_shard_ranges_match_dataloader(wf):
+    for P in (1, 2, 4, 8):
+        N = 1024 * P
+        for causal in (False, True):
+            for r in range(P):
+                a0, a1, b0, b1 = wf.shard_ranges(P, r, N, causal)
+                got = list(range(a0, a1)) + list(range(b0, b1))
+                assert got == list(unit_positions(r, P, N, causal))
+
+
+def test_bad_config_is_config_error(wf):
+    from paper_2407_00611_b200._lib import lib
+    import ctypes
+    h = ctypes.c_void_p()
+    assert lib().wf_init_emulated(8, 3, ctypes.byref(h)) == 2
+    assert b"divide" in lib().wf_last_error(None)
