@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark of the WallFacer hot path on B200: attention forward + backward through
+the C ABI (wf_attn_fwd + wf_attn_bwd of libwf.so), one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--C c] [--seq S] [--workload gpt|dit]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (driver launch for N > 1)
+    python bench.py --impl reference ...                     (the fp64 CPU oracle arm)
+
+A step = one wf_attn_fwd + one wf_attn_bwd over the whole sequence (every row of
+SURVEY.md §8(a)).  Workload (BASELINE.json configs): GPT-style 32 heads x 128, causal,
+N = max(32K, 16K * P) tokens (configs[1] at P <= 2, configs[2] at P = 8); synthetic
+N(0,1) bf16 inputs, resident in HBM.  FLOPs follow the FlashAttention convention
+(fwd 4 N^2 h d, halved if causal; bwd 2.5 x fwd).  value = whole-job TFLOP/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attn fwd+bwd TFLOP/s/GPU & tensor-pipe % vs N at 1/2/4/8 B200, C∈{1,2,4}"
+DEFAULT_C = {1: 1, 2: 2, 4: 2, 8: 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wf", choices=["wf", "reference"])
+    ap.add_argument("--C", type=int, default=0, help="team size (0 = default table)")
+    ap.add_argument("--seq", type=int, default=0, help="sequence length N (0 = workload default)")
+    ap.add_argument("--workload", default="gpt", choices=["gpt", "dit"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args, P):
+    if args.workload == "gpt":
+        heads, hd, causal = 32, 128, True
+        N = args.seq or max(32768, 16384 * P)
+        name = f"GPT-style attention 32x128 causal N={N}"
+    else:
+        heads, hd, causal = 16, 72, False
+        N = args.seq or 65536
+        name = f"DiT-style attention 16x72 full N={N}"
+    return name, N, heads, hd, causal
+
+
+def flops(N, heads, hd, causal):
+    f = 4.0 * N * N * heads * hd * (0.5 if causal else 1.0)
+    return f, 2.5 * f
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason")}
+        flags = {
+            "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
+            "hw_power_brake_slowdown": 0x80, "sync_boost": 0x10, "gpu_idle": 0x1, "applications_clocks_setting": 0x2,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in flags.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+        del names
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_oracle_sample(N_s, heads_s, hd, causal):
+    """Time the fp64 oracle (dense fwd+bwd) on a bounded sample; returns (TFLOP/s, seconds, cores)."""
+    import numpy as np
+    from oracle.dense import attention_bwd
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info() if t.get("user_api") == "blas"] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    rng = np.random.default_rng(0)
+    q, k, v, do = (rng.standard_normal((N_s, heads_s, hd)) for _ in range(4))
+    t0 = time.perf_counter()
+    attention_bwd(q, k, v, do, causal=causal)
+    dt = time.perf_counter() - t0
+    f, b = flops(N_s, heads_s, hd, causal)
+    return (f + b) / dt / 1e12, dt, cores
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle as it stands, on host cores, bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    P = max(1, args.gpus)
+    name, N, heads, hd, causal = workload(args, P)
+    N_s = 8192
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, dt, cores = cpu_oracle_sample(N_s, 1, hd, causal)
+        if i >= args.warmup:
+            vals.append(v)
+    val = statistics.median(vals)
+    sample = f"dense fp64 fwd+bwd, 1 of {heads} heads, N={N_s} of {N} tokens, per step"
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1)",
+           "config": {"workload": name, "N": N, "heads": heads, "head_dim": hd, "causal": causal},
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    P = world
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2407_00611_b200 as wf
+
+    name, N, heads, hd, causal = workload(args, P)
+    C = args.C or DEFAULT_C.get(P, 1)
+    n = N // P
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    shape = (n, heads, hd)
+    q, k, v, do = (torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16) for _ in range(4))
+    ctx = wf.Context(P, C, rank=rank, emulated=False)
+    o = torch.empty_like(q)
+    lse = torch.empty((heads, n), dtype=torch.float32, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.fwd(q, k, v, N, causal, o=o, lse=lse)
+        ctx.bwd(do, q, k, v, o, lse, N, causal, dq=dq, dk=dk, dv=dv)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    ctx.set_profiling(True)
+    ctx.kernel_times()  # reset
+    launches0 = ctx.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches() - launches0
+    fwd_ms, bwd_ms, nf, nb = ctx.kernel_times()
+    ctx.set_profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    ff, fb = flops(N, heads, hd, causal)
+    total_tflops = (ff + fb) * args.steps / (ms / 1e3) / 1e12
+
+    # roofline of the dominant kernel (the block backward: 5 of the 7 GEMM-equivalents)
+    peaks = load_peaks()
+    peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
+    per_gpu_f, per_gpu_b = ff / P, fb / P
+    achieved_b = per_gpu_b * args.steps / (bwd_ms / 1e3) / 1e12 if bwd_ms > 0 else None
+    achieved_f = per_gpu_f * args.steps / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None
+
+    # e2e: host buffers through the same public API, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
+        ho, hdq, hdk, hdv = (torch.empty_like(hq).pin_memory() for _ in range(4))
+        hl = torch.empty((heads, n), dtype=torch.float32).pin_memory()
+        dq2, dk2, dv2, do2 = (torch.empty_like(q) for _ in range(4))
+        q2, k2, v2 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        steps_e = max(2, min(args.steps, 5))
+
+        def e2e_step():
+            q2.copy_(hq, non_blocking=True)
+            k2.copy_(hk, non_blocking=True)
+            v2.copy_(hv, non_blocking=True)
+            do2.copy_(hdo, non_blocking=True)
+            ctx.fwd(q2, k2, v2, N, causal, o=o, lse=lse)
+            ctx.bwd(do2, q2, k2, v2, o, lse, N, causal, dq=dq2, dk=dk2, dv=dv2)
+            ho.copy_(o, non_blocking=True)
+            hl.copy_(lse, non_blocking=True)
+            hdq.copy_(dq2, non_blocking=True)
+            hdk.copy_(dk2, non_blocking=True)
+            hdv.copy_(dv2, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps_e):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        h2d = 4 * q.numel() * 2
+        d2h = 4 * q.numel() * 2 + lse.numel() * 4
+        e2e = {"value": (ff + fb) * steps_e / (el / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": el / steps_e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        N_s = 16384
+        v_cpu, dt, cores = cpu_oracle_sample(N_s, 1, hd, causal)
+        cpu = {"value": v_cpu, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+               "sample": f"dense fp64 fwd+bwd, 1 of {heads} heads, N={N_s} of {N} tokens ({dt:.1f} s)"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": total_tflops, "unit": "TFLOP/s (whole job)", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) bf16, resident in HBM",
+            "config": {"workload": name, "N": N, "heads": heads, "head_dim": hd, "causal": causal, "P": P, "C": C,
+                       "parallelism": f"sp{P} (WallFacer teams of {C})",
+                       "l2": "inputs (4 x N/P x h x d bf16) exceed L2 (126 MB) per step" if q.numel() * 8 > 126e6 else "inputs fit L2"},
+            "tflops_per_gpu": total_tflops / world,
+            "frac_of_peak_per_gpu": total_tflops / world / peak,
+            "fwd_kernel_tflops": achieved_f, "bwd_kernel_tflops": achieved_b,
+            "kernel_ms_per_step": {"block_fwd": fwd_ms / args.steps, "block_bwd": bwd_ms / args.steps},
+            "roofline": {"kernel": "wf_block_bwd_kernel", "bound": "tensor", "achieved": achieved_b, "peak": peak,
+                         "unit": "TFLOP/s", "frac": (achieved_b / peak) if achieved_b else None, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
+                         "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -121,6 +121,13 @@ wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges
 /* Timing aid: number of kernels this context launched since creation. */
 int64_t wf_kernel_launches(const wf_ctx* ctx);
 
+/* Timing aid (bench): when on != 0, CUDA events are recorded on the launching stream
+ * around every block-forward and block-backward kernel.  wf_kernel_times synchronizes
+ * and returns the summed device milliseconds and launch counts since profiling was
+ * enabled (out[0] fwd ms, out[1] bwd ms, out[2] fwd launches, out[3] bwd launches). */
+wf_status wf_set_profiling(wf_ctx* ctx, int on);
+wf_status wf_kernel_times(wf_ctx* ctx, double out[4]);
+
 /* Last error text of ctx (or of the last context-less call when ctx is NULL). */
 const char* wf_last_error(const wf_ctx* ctx);
 

@@ -24,7 +24,7 @@ Messages go through a mailbox network: every receive must match a send with the
 same (kind, step, src, dst) and the network must be empty at the end
 (quiescence).  A record (pass, kind, step, src, dst, block, bytes)
 is emitted for every message with src != dst (self-sends are local, reading c4).
-Byte widths (reading c17): Q/K/V/dO/partial-O bf16 (2 B); LSE, D and the
+Byte widths (reading c17): Q/K/V/dO bf16 (2 B); partial O, LSE, D and the
 dQ/dK/dV partials fp32 (4 B).  Step numbering: -1 gathers and init shuffle;
 s in [0, R-2] for the hop after compute step s; R-1 for RET_DQ; R for the
 post-loop reductions.  Block ids: see DESIGN.md "CommTrace".
@@ -178,7 +178,7 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
                 po, pl = _rows_of_member(o, j, n), l[:, j * n:(j + 1) * n]
             else:
                 po = pl = None
-            net.send(0, "RS_O", R, r, p, p, n * E * 2, po)
+            net.send(0, "RS_O", R, r, p, p, n * E * 4, po)
             net.send(0, "RS_LSE", R, r, p, p, n * h * 4, pl)
     O = np.zeros((N, h, d)) if compute else None
     LSE = np.full((h, N), -np.inf) if compute else None

@@ -76,7 +76,7 @@ namespace wf {
 // ReduceScatter_combine of the C partial (O, lse) states of this rank's rows.
 struct MergeArgs {
   int rows, heads, D, nparts;
-  const __nv_bfloat16* o[WF_MAX_PARTS];   // [rows, heads, D] each
+  const float* o[WF_MAX_PARTS];           // fp32 [rows, heads, D] each
   const float* lse[WF_MAX_PARTS];         // lse[j][head * lse_stride[j] + row]
   int64_t lse_stride[WF_MAX_PARTS];
   __nv_bfloat16* out;                     // [rows, heads, D]

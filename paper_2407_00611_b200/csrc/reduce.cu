@@ -47,10 +47,16 @@ __global__ void wf_merge_kernel(MergeArgs a) {
       for (int j = 0; j < WF_MAX_PARTS; ++j) {
         if (j < a.nparts && l[j] != -INFINITY) {
           const float w = __expf(l[j] - Lf);
-          const uint4 v = *reinterpret_cast<const uint4*>(a.o[j] + static_cast<int64_t>(row) * a.heads * a.D + e0);
-          const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = fmaf(w, bf2f(h[i]), acc[i]);
+          const float4* src = reinterpret_cast<const float4*>(a.o[j] + static_cast<int64_t>(row) * a.heads * a.D + e0);
+          const float4 v0 = src[0], v1 = src[1];
+          acc[0] = fmaf(w, v0.x, acc[0]);
+          acc[1] = fmaf(w, v0.y, acc[1]);
+          acc[2] = fmaf(w, v0.z, acc[2]);
+          acc[3] = fmaf(w, v0.w, acc[3]);
+          acc[4] = fmaf(w, v1.x, acc[4]);
+          acc[5] = fmaf(w, v1.y, acc[5]);
+          acc[6] = fmaf(w, v1.z, acc[6]);
+          acc[7] = fmaf(w, v1.w, acc[7]);
         }
       }
     }

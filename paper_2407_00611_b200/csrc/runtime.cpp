@@ -44,8 +44,7 @@ struct RankBufs {
   bf16 *qt = nullptr, *kt = nullptr, *vt = nullptr;  // team Q/K/V (C*n rows)
   bf16 *rk[2] = {nullptr, nullptr}, *rv[2] = {nullptr, nullptr};  // ring / slice K,V (Bk rows)
   float *o_state = nullptr, *lse_state = nullptr;    // fp32 (C*n rows), lse [C][h][n]
-  bf16* o_part = nullptr;                            // bf16 partial O (C*n rows)
-  bf16* rs_o = nullptr;                              // [C][n rows] partials of my rows
+  float* rs_o = nullptr;                             // [C][n rows] fp32 partials of my rows
   float* rs_lse = nullptr;                           // [C][h][n]
   // backward
   float* dsum = nullptr;                             // [h][n]
@@ -91,6 +90,10 @@ struct wf_ctx {
   std::vector<wf_event> trace_fwd, trace_bwd;
   int64_t launches = 0;
   std::string err;
+  // kernel timing (bench)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_fwd, ev_bwd;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
@@ -198,8 +201,7 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
       add(&b.t_do, team * 2);
       add(&b.t_lse, C * h * n * 4);
       add(&b.t_dsum, C * h * n * 4);
-      add(&b.o_part, team * 2);
-      add(&b.rs_o, team * 2);
+      add(&b.rs_o, team * 4);
       add(&b.rs_lse, C * h * n * 4);
       add(&b.rsq, team * 4);
       if (g.paper) {
@@ -295,6 +297,30 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
 template <typename T>
 T* at(T* base, int64_t off) {
   return base ? base + off : nullptr;
+}
+
+cudaEvent_t pool_event(wf_ctx* ctx) {
+  cudaEvent_t e = nullptr;
+  if (!ctx->ev_pool.empty()) {
+    e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+cudaEvent_t prof_begin(wf_ctx* ctx, cudaStream_t st) {
+  if (!ctx->profiling) return nullptr;
+  cudaEvent_t e = pool_event(ctx);
+  cudaEventRecord(e, st);
+  return e;
+}
+void prof_end(wf_ctx* ctx, cudaStream_t st, cudaEvent_t e0,
+              std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+  if (!ctx->profiling || !e0) return;
+  cudaEvent_t e1 = pool_event(ctx);
+  cudaEventRecord(e1, st);
+  v.push_back({e0, e1});
 }
 
 wf_status kcheck(wf_ctx* ctx, cudaError_t e, const char* what) {
@@ -410,8 +436,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
     } else if (C == 1) {  // final output
       a.o_out_bf16 = Oout(r);
       a.lse_out = Lout(r);
-    } else {  // this member's partial for the team rows
-      a.o_out_bf16 = b.o_part;
+    } else {  // this member's fp32 partial for the team rows (reading c17)
+      a.o_out_f32 = b.o_state;
       a.lse_out = b.lse_state;
     }
     if (ctx->dry) return WF_OK;
@@ -419,7 +445,10 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
     if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
         !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
       return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
-    return kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
+    cudaEvent_t e0 = prof_begin(ctx, st);
+    wf_status ks = kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
+    prof_end(ctx, st, e0, ctx->ev_fwd);
+    return ks;
   };
   if (overlap) CK(cudaEventRecord(ctx->ev_a, st));  // slot 0 ready
   for (int s = 0; s < R; ++s) {
@@ -459,7 +488,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (p == r) continue;
         const int jp = p - t * C;
         Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}};
-        x.segs.push_back({at(lp(r, B(ctx, r).o_part), jp * n * E), at(lp(p, B(ctx, p).rs_o), j * n * E), n * E * 2});
+        x.segs.push_back({at(lp(r, B(ctx, r).o_state), jp * n * E), at(lp(p, B(ctx, p).rs_o), j * n * E), n * E * 4});
         xs.push_back(x);
         Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}};
         y.segs.push_back({at(lp(r, B(ctx, r).lse_state), jp * h * n), at(lp(p, B(ctx, p).rs_lse), j * h * n), h * n * 4});
@@ -477,7 +506,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       m.D = g.d;
       m.nparts = C;
       for (int i = 0; i < C; ++i) {
-        m.o[i] = i == j ? b.o_part + i * n * E : b.rs_o + i * n * E;
+        m.o[i] = i == j ? b.o_state + i * n * E : b.rs_o + i * n * E;
         m.lse[i] = i == j ? b.lse_state + i * h * n : b.rs_lse + i * h * n;
         m.lse_stride[i] = n;
       }
@@ -627,7 +656,9 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
           !make_tmap_rows(&tv, sv[r], a.nk, g.h, g.d) || !make_tmap_rows(&tdo, pdo(r, s), a.nq, g.h, g.d))
         return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+      cudaEvent_t e0 = prof_begin(ctx, st);
       WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, a, g.d, st), "block_bwd"));
+      prof_end(ctx, st, e0, ctx->ev_bwd);
     }
     if (s < R - 1) {
       if (overlap) {
@@ -957,6 +988,32 @@ wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges
 
 int64_t wf_kernel_launches(const wf_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+wf_status wf_set_profiling(wf_ctx* ctx, int on) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  ctx->profiling = on != 0;
+  return WF_OK;
+}
+
+wf_status wf_kernel_times(wf_ctx* ctx, double out[4]) {
+  if (!ctx || !out) return fail(ctx, WF_ERR_ARG, "wf_kernel_times: null");
+  CK(cudaDeviceSynchronize());
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* lists[2] = {&ctx->ev_fwd, &ctx->ev_bwd};
+  for (int i = 0; i < 2; ++i) {
+    double ms = 0;
+    for (auto& pr : *lists[i]) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, pr.first, pr.second));
+      ms += t;
+      ctx->ev_pool.push_back(pr.first);
+      ctx->ev_pool.push_back(pr.second);
+    }
+    out[i] = ms;
+    out[2 + i] = static_cast<double>(lists[i]->size());
+    lists[i]->clear();
+  }
+  return WF_OK;
+}
+
 const char* wf_last_error(const wf_ctx* ctx) {
   if (ctx) return ctx->err.c_str();
   if (!g_ctxless_err.empty()) return g_ctxless_err.c_str();
@@ -973,6 +1030,9 @@ wf_status wf_finalize(wf_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  for (auto& pr : ctx->ev_fwd) ctx->ev_pool.push_back(pr.first), ctx->ev_pool.push_back(pr.second);
+  for (auto& pr : ctx->ev_bwd) ctx->ev_pool.push_back(pr.first), ctx->ev_pool.push_back(pr.second);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
   return WF_OK;
 }

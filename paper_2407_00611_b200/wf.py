@@ -150,6 +150,15 @@ class Context:
         _check(lib().wf_get_trace(self.h, buf, n.value, ctypes.byref(n)), self.h)
         return _events(buf, n.value)
 
+    def set_profiling(self, on=True):
+        _check(lib().wf_set_profiling(self.h, int(on)), self.h)
+
+    def kernel_times(self):
+        """(fwd_ms, bwd_ms, fwd_launches, bwd_launches) since profiling was enabled / last call."""
+        out = (ctypes.c_double * 4)()
+        _check(lib().wf_kernel_times(self.h, out), self.h)
+        return out[0], out[1], int(out[2]), int(out[3])
+
     def kernel_launches(self):
         return int(lib().wf_kernel_launches(self.h))
 
