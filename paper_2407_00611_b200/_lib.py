@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwf.so")
+LIB_PATH = os.environ.get("WF_LIB_PATH") or os.path.join(_HERE, "libwf.so")
 
 c_int, c_i64, c_p, c_f = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
 c_i32p = ctypes.POINTER(ctypes.c_int32)

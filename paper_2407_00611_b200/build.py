@@ -44,8 +44,12 @@ def _run(cmd, verbose):
         sys.stderr.write(r.stdout + r.stderr)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib=None, obj=None) -> str:
+    """Build libwf.so; `defines` (e.g. ["WF_DQ_MODE=0"]) and lib/obj paths make experiment variants."""
+    OBJ_ = obj or OBJ
+    LIB_ = lib or LIB
+    os.makedirs(OBJ_, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     nccl_inc, nccl_lib = _nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
@@ -53,15 +57,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
     hdr_mtime = max(os.path.getmtime(h) for h in headers) if headers else 0
     objs = []
     for s in srcs:
-        o = os.path.join(OBJ, os.path.basename(s) + ".o")
+        o = os.path.join(OBJ_, os.path.basename(s) + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_mtime):
             extra = ["-Xptxas", "-v"] if verbose and s.endswith(".cu") else []
-            _run([NVCC] + CFLAGS + ["-I" + nccl_inc] + extra + ["-c", s, "-o", o], verbose)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
+            _run([NVCC] + CFLAGS + dflags + ["-I" + nccl_inc] + extra + ["-c", s, "-o", o], verbose)
+    if force or not os.path.exists(LIB_) or os.path.getmtime(LIB_) < max(os.path.getmtime(o) for o in objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB_] + objs +
              ["-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib, "-lcudart"], verbose)
-    return LIB
+    return LIB_
 
 
 if __name__ == "__main__":

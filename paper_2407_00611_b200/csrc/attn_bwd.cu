@@ -9,8 +9,9 @@
 //   dP^T = V dO^T, dS^T = P^T o (dP^T - D), dK += dS^T Q / sqrt(d), dQ += dS K / sqrt(d).
 //
 // CTA per (128-row K/V tile, head); it loops over the visible 128-row query tiles.
-// 10 warps: 0-3 dQ drain (TMEM -> fp32 atomics, lane = query row), 4-7 compute
-// (lane = key row), 8 TMA producer, 9 TMEM allocator + MMA issuer.
+// 14 warps: 0-3 dQ drain (TMEM -> smem -> bulk reduce-add into fp32 dQ, lane = query
+// row), 4-11 compute (lane = key row, two warps per lane quadrant split the 128 query
+// columns), 12 TMA producer, 13 TMEM allocator + MMA issuer.
 // TMEM: S^T [0,128) (P^T bf16 over [0,64)), dV [128,128+DP), dP^T [256,384)
 // (dS^T bf16 over [256,320), then dQ over [256,256+DP)), dK [384,384+DP).
 #include "common.h"
@@ -34,6 +35,9 @@ __device__ __forceinline__ int qtile_kind(const BwdArgs& a, int kpos0, int it) {
   return qp0 < kpos0 ? 0 : (qp0 == kpos0 ? 2 : 1);
 }
 
+constexpr int kStgBuf = 128 * 128;       // one dQ staging buffer: [128 rows][32 fp32], 128B-swizzled
+constexpr int kStgBufs = 2;
+
 template <int D>
 struct BwdCfg {
   static constexpr int DP = (D + 15) / 16 * 16;
@@ -45,9 +49,11 @@ struct BwdCfg {
   static constexpr int OFF_Q = 2 * TILE;        // 2 stages
   static constexpr int OFF_DO = 4 * TILE;       // 1 stage
   static constexpr int OFF_DS = 5 * TILE;       // [128 q] x [128 kv] bf16, MN-major SW128 (2 panels)
-  static constexpr int OFF_STAT = OFF_DS + 2 * PANEL;  // 2 stages x (lse[128], dsum[128]) fp32
+  static constexpr int OFF_STG = OFF_DS + 2 * PANEL;   // dQ staging: kStgBufs x [128 rows][32 fp32]
+  static constexpr int OFF_STAT = OFF_STG + kStgBufs * kStgBuf;  // 2 stages x (lse[128], dsum[128]) fp32
   static constexpr int OFF_BAR = OFF_STAT + 2 * 1024;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int SMEM = OFF_BAR + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 enum {
@@ -55,19 +61,46 @@ enum {
   B_DQE = 12, B_DSE = 13, B_DONE = 14, B_NUM = 15
 };
 
+constexpr int kThreads = 14 * 32;  // 4 dQ-drain + 8 compute + TMA + MMA warps
+constexpr int kCompute = 256;
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// global[dst, dst + bytes) += shared[src, src + bytes) (fp32), completed per bulk group
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+// TMA tensor reduce-add of a [128 rows][32 fp32] SW128 smem box into global (fp32)
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* ssrc, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(ssrc)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 
 template <int D>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
     wf_block_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                        const __grid_constant__ BwdArgs a) {
+                        const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ BwdArgs a) {
   using Cfg = BwdCfg<D>;
   constexpr int DP = Cfg::DP;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BAR + B_NUM * 8);
   float* stat = reinterpret_cast<float*>(smem + Cfg::OFF_STAT);  // [stage][2][128]
@@ -81,6 +114,7 @@ __global__ void __maxnreg__(200)
   const int nqt = a.nq / WF_TILE;
 
   if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
     mbar_init(&bar[B_KV], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar[B_QF + i], 1);
@@ -90,15 +124,15 @@ __global__ void __maxnreg__(200)
     mbar_init(&bar[B_DOE], 1);
     mbar_init(&bar[B_S], 1);
     mbar_init(&bar[B_DP], 1);
-    mbar_init(&bar[B_P], 128);
-    mbar_init(&bar[B_DS], 128);
+    mbar_init(&bar[B_P], kCompute);
+    mbar_init(&bar[B_DS], kCompute);
     mbar_init(&bar[B_DQF], 1);
     mbar_init(&bar[B_DQE], 128);
     mbar_init(&bar[B_DSE], 1);
     mbar_init(&bar[B_DONE], 1);
     fence_barrier_init();
   }
-  if (warp == 9) {
+  if (warp == 13) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
@@ -107,7 +141,7 @@ __global__ void __maxnreg__(200)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       tma_prefetch_desc(&tmQ);
@@ -138,8 +172,11 @@ __global__ void __maxnreg__(200)
         ++ii;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
+    // Order per query tile i: dP_i, [P_i] dV_i, S_{i+1}, [dS_i] dK_i, dQ_i.  S_{i+1} is
+    // issued as soon as dV_i has consumed P_i from TMEM, so the compute warps' exp work
+    // of tile i+1 overlaps the dK_i / dQ_i MMAs.
     if (lane == 0) {
       constexpr uint32_t idSP = idesc_bf16_f32(128, 128, 0, 0);   // K x Q^T, V x dO^T (both K-major)
       constexpr uint32_t idKV = idesc_bf16_f32(128, DP, 0, 1);    // P^T/dS^T (TMEM) x dO/Q (MN-major)
@@ -148,15 +185,10 @@ __global__ void __maxnreg__(200)
       const uint32_t sV = smem_u32(smem + Cfg::OFF_V);
       const uint32_t sDO = smem_u32(smem + Cfg::OFF_DO);
       const uint32_t sDS = smem_u32(smem + Cfg::OFF_DS);
-      mbar_wait(&bar[B_KV], 0);
-      tc_fence_after();
-      int ii = 0;
-      for (int it = 0; it < nqt; ++it) {
-        if (qtile_kind(a, kpos0, it) == 0) continue;
-        const int st = ii & 1;
+      auto issue_s = [&](int i) {
+        const int st = i & 1;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
-        // S^T = K Q^T
-        mbar_wait(&bar[B_QF + st], (ii >> 1) & 1);
+        mbar_wait(&bar[B_QF + st], (i >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
@@ -165,7 +197,16 @@ __global__ void __maxnreg__(200)
                  smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024), idSP, k > 0 ? 1u : 0u);
         }
         mma_commit(&bar[B_S]);
-        // dP^T = V dO^T  (dP region must be drained of the previous dQ)
+      };
+      int ntiles = 0;
+      for (int it = 0; it < nqt; ++it) ntiles += qtile_kind(a, kpos0, it) != 0;
+      mbar_wait(&bar[B_KV], 0);
+      tc_fence_after();
+      if (ntiles > 0) issue_s(0);
+      for (int ii = 0; ii < ntiles; ++ii) {
+        const int st = ii & 1;
+        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
+        // dP^T = V dO^T (the dP region must be drained of the previous dQ)
         mbar_wait(&bar[B_DOF], ii & 1);
         if (ii >= 1) mbar_wait(&bar[B_DQE], (ii - 1) & 1);
         tc_fence_after();
@@ -184,6 +225,7 @@ __global__ void __maxnreg__(200)
           mma_ts(tbase + 128, tbase + 0 + k * 8, smem_desc_sw128(sDO + k * 2048, Cfg::PANEL, 1024), idKV,
                  (ii > 0 || k > 0) ? 1u : 0u);
         mma_commit(&bar[B_DOE]);
+        if (ii + 1 < ntiles) issue_s(ii + 1);
         // dK += dS^T Q ; dQ = dS K
         mbar_wait(&bar[B_DS], ii & 1);
         tc_fence_after();
@@ -198,85 +240,83 @@ __global__ void __maxnreg__(200)
                  smem_desc_sw128(sK + k * 2048, Cfg::PANEL, 1024), idQ, k > 0 ? 1u : 0u);
         mma_commit(&bar[B_DQF]);
         mma_commit(&bar[B_DSE]);
-        ++ii;
       }
       mma_commit(&bar[B_DONE]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ compute: P^T, dS^T
+    // 8 warps: warp w covers TMEM lane quadrant w % 4 (key rows) and query columns
+    // [64 h, 64 h + 64), h = (w - 4) / 4.
     const int wq = warp & 3;
+    const int hf = (warp - 4) >> 2;
     const int r = wq * 32 + lane;  // key row within the tile
     const uint32_t tl = tbase + (static_cast<uint32_t>(wq * 32) << 16);
-    uint8_t* sds = smem + Cfg::OFF_DS;
+    uint8_t* sds = smem + Cfg::OFF_DS + hf * Cfg::PANEL + (r >> 3) * 1024 + (r & 7) * 128;
     int ii = 0;
     for (int it = 0; it < nqt; ++it) {
       const int kind = qtile_kind(a, kpos0, it);
       if (kind == 0) continue;
       const int st = ii & 1;
-      const float* slse = stat + st * 256;
-      const float* sdd = slse + 128;
+      const float* slse = stat + st * 256 + hf * 64;
+      const float* sdd = stat + st * 256 + 128 + hf * 64;
       mbar_wait(&bar[B_QF + st], (ii >> 1) & 1);  // stats landed
       mbar_wait(&bar[B_S], ii & 1);
       tc_fence_after();
+      uint32_t pk[32];  // P^T row, this half: 64 bf16
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t rr[32];
-        tmem_ld32(tl + c * 32, rr);
+        tmem_ld32(tl + hf * 64 + c * 32, rr);
         tmem_wait_ld();
-        float p[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int q = c * 32 + i;
-          const float lq = slse[q];
-          float e = fast_exp2(fmaf(__uint_as_float(rr[i]), a.scale_log2, -lq * kLog2e));
-          if (lq == -INFINITY || (kind == 2 && q < r)) e = 0.f;
-          p[i] = e;
+        for (int i = 0; i < 16; ++i) {
+          float e[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = c * 32 + 2 * i + u;  // column within this half
+            const float lq = slse[q];
+            e[u] = fast_exp2(fmaf(__uint_as_float(rr[2 * i + u]), a.scale_log2, -lq * kLog2e));
+            if (lq == -INFINITY || (kind == 2 && hf * 64 + q < r)) e[u] = 0.f;
+          }
+          pk[c * 16 + i] = pack_bf16x2(e[0], e[1]);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(p[2 * i], p[2 * i + 1]);
-        tmem_st16(tl + c * 16, pk);
       }
+      tmem_st32(tl + hf * 32, pk);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar[B_P]);
-      // dS^T = P^T o (dP^T - D)
+      // dS^T = P^T o (dP^T - D), pre-scaled by 1/sqrt(d) for both dK and dQ
       mbar_wait(&bar[B_DP], ii & 1);
       tc_fence_after();
-      // dS^T -> TMEM (A of dK += dS^T Q), dS -> smem (A of dQ = dS K, MN-major).
-      // P^T is re-read as the bf16 copy already in TMEM (keeps 128 fp32 registers free).
       if (ii >= 1) mbar_wait(&bar[B_DSE], (ii - 1) & 1);
+      uint32_t dk[32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rr[32], pb[16];
-        tmem_ld32(tl + 256 + c * 32, rr);
-        tmem_ld16(tl + c * 16, pb);
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tl + 256 + hf * 64 + c * 32, rr);
         tmem_wait_ld();
-        uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pb[i]));
-          const float d0 = pf.x * (__uint_as_float(rr[2 * i]) - sdd[c * 32 + 2 * i]);
-          const float d1 = pf.y * (__uint_as_float(rr[2 * i + 1]) - sdd[c * 32 + 2 * i + 1]);
-          pk[i] = pack_bf16x2(d0, d1);
-        }
-        tmem_st16(tl + 256 + c * 16, pk);
-        // 32 q values = 4 chunks of 16 B in panel (c >> 1), chunks (c & 1) * 4 + j
-        uint8_t* rowp = sds + (c >> 1) * Cfg::PANEL + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int chunk = (c & 1) * 4 + j;
-          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c * 16 + i]));
+          const int q = c * 32 + 2 * i;
+          const float d0 = pf.x * (__uint_as_float(rr[2 * i]) - sdd[q]) * a.scale;
+          const float d1 = pf.y * (__uint_as_float(rr[2 * i + 1]) - sdd[q + 1]) * a.scale;
+          dk[c * 16 + i] = pack_bf16x2(d0, d1);
         }
       }
+      tmem_st32(tl + 256 + hf * 32, dk);
+      // dS -> smem (A of dQ = dS K, MN-major SW128): this half's 64 q = panel hf, row r
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<uint4*>(sds + ((j ^ (r & 7)) << 4)) =
+            make_uint4(dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       fence_proxy_async_smem();
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar[B_DS]);
       ++ii;
     }
-    // epilogue: dK (scaled), dV of this key tile
+    // epilogue: dK, dV of this key tile (this warp's half of the 16-column chunks)
     mbar_wait(&bar[B_DONE], 0);
     tc_fence_after();
     const int grow = k0 + r;
@@ -285,25 +325,49 @@ __global__ void __maxnreg__(200)
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t col0 = which == 0 ? 384 : 128;
-      const float sc = which == 0 ? a.scale : 1.f;
       float* acc = which == 0 ? a.dk_acc : a.dv_acc;
       __nv_bfloat16* outb = which == 0 ? a.dk_out : a.dv_out;
 #pragma unroll
-      for (int c = 0; c < DP / 16; ++c) {
+      for (int c = hf; c < DP / 16; c += 2) {
         uint32_t rr[16];
         if (any) {
           tmem_ld16(tl + col0 + c * 16, rr);
           tmem_wait_ld();
         }
+        float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c * 16 + i;
-          if (col < D) {
-            const float v = any ? __uint_as_float(rr[i]) * sc : 0.f;
-            if (outb) {
-              outb[orow + col] = __float2bfloat16_rn(v);
-            } else if (acc) {
-              acc[orow + col] = a.dkv_accumulate ? acc[orow + col] + v : v;
+        for (int i = 0; i < 16; ++i) v[i] = any ? __uint_as_float(rr[i]) : 0.f;
+        if (c * 16 + 16 <= D) {
+          if (outb) {
+            uint4* dst = reinterpret_cast<uint4*>(outb + orow + c * 16);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                  pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(acc + orow + c * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float4 x = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              if (a.dkv_accumulate) {
+                const float4 y = dst[i];
+                x.x += y.x;
+                x.y += y.y;
+                x.z += y.z;
+                x.w += y.w;
+              }
+              dst[i] = x;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = c * 16 + i;
+            if (col < D) {
+              if (outb)
+                outb[orow + col] = __float2bfloat16_rn(v[i]);
+              else
+                acc[orow + col] = a.dkv_accumulate ? acc[orow + col] + v[i] : v[i];
             }
           }
         }
@@ -311,39 +375,80 @@ __global__ void __maxnreg__(200)
     }
   } else {
     // ------------------------------------------------------------ dQ drain (warps 0-3)
+    // TMEM -> registers -> this thread's 128-byte staging row -> bulk reduce-add into the
+    // fp32 dQ accumulator in global memory (one full-line L2 reduction per row chunk).
     const int r = warp * 32 + lane;  // query row within the tile
     const uint32_t tl = tbase + (static_cast<uint32_t>(warp * 32) << 16);
-    int ii = 0;
+#ifndef WF_DQ_MODE
+#define WF_DQ_MODE 3
+#endif
+    // Each thread writes its query row's 32 columns into a 128B-swizzled staging row
+    // (16-byte chunk j at j ^ (r & 7): conflict-free), then one thread reduce-adds the
+    // [128 x 32] box into the fp32 dQ accumulator with a TMA tensor reduction.
+    uint8_t* stg_row = smem + Cfg::OFF_STG + r * 128;
+    int ii = 0, chunk = 0;
     for (int it = 0; it < nqt; ++it) {
       if (qtile_kind(a, kpos0, it) == 0) continue;
       mbar_wait(&bar[B_DQF], ii & 1);
       tc_fence_after();
+#if WF_DQ_MODE == 0
       float* dst = a.dq_acc + (static_cast<size_t>(it * WF_TILE + r) * a.heads + head) * D;
+#endif
 #pragma unroll
-      for (int c = 0; c < DP / 16; ++c) {
-        uint32_t rr[16];
-        tmem_ld16(tl + 256 + c * 16, rr);
+      for (int c0 = 0; c0 < DP; c0 += 32, ++chunk) {
+        uint32_t rr[32];
+        if (c0 + 32 <= DP) {
+          tmem_ld32(tl + 256 + c0, rr);
+        } else {
+          uint32_t r16[16];
+          tmem_ld16(tl + 256 + c0, r16);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) rr[i] = r16[i];
+#pragma unroll
+          for (int i = 16; i < 32; ++i) rr[i] = 0u;
+        }
         tmem_wait_ld();
+        if (c0 + 32 >= DP) {  // last TMEM read of this tile: release the dQ region
+          tc_fence_before();
+          mbar_arrive(&bar[B_DQE]);
+        }
+#if WF_DQ_MODE == 3
+        uint8_t* stg = stg_row + (chunk & 1) * kStgBuf;
+        if (threadIdx.x == 0) bulk_wait_read<1>();  // reduce of chunk-2 has read this buffer
+        named_bar_sync(1, 128);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (c * 16 + 4 * j < D)
-            atomicAdd(reinterpret_cast<float4*>(dst + c * 16) + j,
-                      make_float4(__uint_as_float(rr[4 * j]) * a.scale, __uint_as_float(rr[4 * j + 1]) * a.scale,
-                                  __uint_as_float(rr[4 * j + 2]) * a.scale, __uint_as_float(rr[4 * j + 3]) * a.scale));
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(stg + ((j ^ (r & 7)) << 4)) =
+              make_uint4(rr[4 * j], rr[4 * j + 1], rr[4 * j + 2], rr[4 * j + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 0) {
+          tma_reduce_add_3d(&tmDQ, smem + Cfg::OFF_STG + (chunk & 1) * kStgBuf, c0, head, it * WF_TILE);
+          bulk_commit();
+        }
+#else
+        const int ncol = (D - c0) < 32 ? (D - c0) : 32;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j * 4 < ncol)
+            atomicAdd(reinterpret_cast<float4*>(dst + c0) + j,
+                      make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                  __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3])));
+        (void)stg_row;
+#endif
       }
-      tc_fence_before();
-      mbar_arrive(&bar[B_DQE]);
       ++ii;
     }
+    if (threadIdx.x == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc(tbase, 512);
+  if (warp == 13) tmem_dealloc(tbase, 512);
 }
 
 template <int D>
 cudaError_t launch_bwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                         const CUtensorMap& tdo, const BwdArgs& a, cudaStream_t s) {
+                         const CUtensorMap& tdo, const CUtensorMap& tdq, const BwdArgs& a, cudaStream_t s) {
   using Cfg = BwdCfg<D>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -352,7 +457,7 @@ cudaError_t launch_bwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr_set = true;
   }
   dim3 grid(a.nk / WF_TILE, a.heads);
-  wf_block_bwd_kernel<D><<<grid, 320, Cfg::SMEM, s>>>(tq, tk, tv, tdo, a);
+  wf_block_bwd_kernel<D><<<grid, kThreads, Cfg::SMEM, s>>>(tq, tk, tv, tdo, tdq, a);
   return cudaGetLastError();
 }
 
@@ -361,10 +466,12 @@ cudaError_t launch_bwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                              const CUtensorMap& tdo, const BwdArgs& a, int D, cudaStream_t s) {
   if (a.nq % WF_TILE || a.nk <= 0 || a.nk % WF_TILE) return cudaErrorInvalidValue;
+  CUtensorMap tdq;
+  if (!make_tmap_f32_rows(&tdq, a.dq_acc, a.nq > 0 ? a.nq : WF_TILE, a.heads, D)) return cudaErrorInvalidValue;
   switch (D) {
-    case 128: return launch_bwd_d<128>(tq, tk, tv, tdo, a, s);
-    case 64: return launch_bwd_d<64>(tq, tk, tv, tdo, a, s);
-    case 72: return launch_bwd_d<72>(tq, tk, tv, tdo, a, s);
+    case 128: return launch_bwd_d<128>(tq, tk, tv, tdo, tdq, a, s);
+    case 64: return launch_bwd_d<64>(tq, tk, tv, tdo, tdq, a, s);
+    case 72: return launch_bwd_d<72>(tq, tk, tv, tdo, tdq, a, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -42,6 +42,19 @@ bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads,
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 4, static_cast<cuuint64_t>(heads) * D * 4};
+  cuuint32_t box[3] = {32, 1, WF_TILE};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool fill_postable(PosTable* t, int rows, int chunk, const int32_t* starts, int n) {
   std::memset(t, 0, sizeof(*t));
   if (chunk <= 0) {  // contiguous [0, rows)

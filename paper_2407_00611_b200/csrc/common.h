@@ -63,6 +63,8 @@ struct BwdArgs {
 
 // Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.
 bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
+// Host: 3-D TMA map over a [rows, heads, D] fp32 tensor, box {32, 1, 128}, SW128 (dQ reduce-add).
+bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
