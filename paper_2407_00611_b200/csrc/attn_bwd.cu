@@ -260,6 +260,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* slse = stat + st * 256 + hf * 64;
       const float* sdd = stat + st * 256 + 128 + hf * 64;
       mbar_wait(&bar[B_QF + st], (ii >> 1) & 1);  // stats landed
+      {
+        // convert the tile's statistics once: lse -> lse * log2(e) (+inf for query rows
+        // with no key at all, so exp2 gives 0 without a branch), D -> D / sqrt(d)
+        float* sst = stat + st * 256;
+        const int tc = threadIdx.x - 128;
+        const float x = sst[tc];
+        sst[tc] = tc < 128 ? (x == -INFINITY ? INFINITY : x * kLog2e) : x * a.scale;
+        named_bar_sync(2, kCompute);
+      }
       mbar_wait(&bar[B_S], ii & 1);
       tc_fence_after();
       uint32_t pk[32];  // P^T row, this half: 64 bf16
@@ -268,17 +277,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t rr[32];
         tmem_ld32(tl + hf * 64 + c * 32, rr);
         tmem_wait_ld();
+        if (kind == 2) {  // diagonal tile: key r is visible to query column q iff r <= q
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float e[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int q = c * 32 + 2 * i + u;  // column within this half
-            const float lq = slse[q];
-            e[u] = fast_exp2(fmaf(__uint_as_float(rr[2 * i + u]), a.scale_log2, -lq * kLog2e));
-            if (lq == -INFINITY || (kind == 2 && hf * 64 + q < r)) e[u] = 0.f;
+          for (int i = 0; i < 16; ++i) {
+            const int q = c * 32 + 2 * i;
+            float e0 = fast_exp2(fmaf(__uint_as_float(rr[2 * i]), a.scale_log2, -slse[q]));
+            float e1 = fast_exp2(fmaf(__uint_as_float(rr[2 * i + 1]), a.scale_log2, -slse[q + 1]));
+            if (hf * 64 + q < r) e0 = 0.f;
+            if (hf * 64 + q + 1 < r) e1 = 0.f;
+            pk[c * 16 + i] = pack_bf16x2(e0, e1);
           }
-          pk[c * 16 + i] = pack_bf16x2(e[0], e[1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int q = c * 32 + 2 * i;
+            pk[c * 16 + i] = pack_bf16x2(fast_exp2(fmaf(__uint_as_float(rr[2 * i]), a.scale_log2, -slse[q])),
+                                         fast_exp2(fmaf(__uint_as_float(rr[2 * i + 1]), a.scale_log2, -slse[q + 1])));
+          }
         }
       }
       tmem_st32(tl + hf * 32, pk);
@@ -299,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c * 16 + i]));
           const int q = c * 32 + 2 * i;
-          const float d0 = pf.x * (__uint_as_float(rr[2 * i]) - sdd[q]) * a.scale;
-          const float d1 = pf.y * (__uint_as_float(rr[2 * i + 1]) - sdd[q + 1]) * a.scale;
+          const float d0 = pf.x * fmaf(__uint_as_float(rr[2 * i]), a.scale, -sdd[q]);
+          const float d1 = pf.y * fmaf(__uint_as_float(rr[2 * i + 1]), a.scale, -sdd[q + 1]);
           dk[c * 16 + i] = pack_bf16x2(d0, d1);
         }
       }

@@ -10,9 +10,10 @@
 // 128-aligned ranges, so a (q tile, k tile) pair is either fully visible, fully
 // masked (skipped) or the diagonal.
 //
-// CTA = 6 warps: warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
-// issuer, warps 2..5 softmax/epilogue (thread <-> TMEM lane <-> query row).
-// TMEM: S double buffer at cols [0,128) and [128,256); O at [256, 256+DP).
+// CTA = 12 warps and two 128-row query tiles: warp 0 TMA producer, warp 1 TMEM allocator +
+// single-thread MMA issuer, warps 4-7 / 8-11 softmax + epilogue of tile 0 / tile 1
+// (thread <-> TMEM lane <-> query row).  TMEM: S_0 [0,128), S_1 [128,256) (P_t written
+// back over S_t as bf16), O_0 [256,256+DP), O_1 [384,384+DP).
 #include "common.h"
 #include "sm100.cuh"
 
@@ -41,38 +42,57 @@ struct FwdCfg {
   static constexpr int NP = (D + 63) / 64;        // 64-column smem panels per tile
   static constexpr int PANEL = 128 * 128;         // bytes of one [128 rows x 64 bf16] panel
   static constexpr int TILE = NP * PANEL;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = TILE;
-  static constexpr int OFF_V = 3 * TILE;
-  static constexpr int OFF_BAR = 5 * TILE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;  // + alignment slack
+  static constexpr int OFF_Q = 0;                 // 2 query tiles
+  static constexpr int OFF_K = 2 * TILE;          // 2 stages
+  static constexpr int OFF_V = 4 * TILE;          // 2 stages
+  static constexpr int OFF_BAR = 6 * TILE;
+  static constexpr int SMEM = OFF_BAR + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-enum { B_Q = 0, B_K = 1, B_V = 3, B_KVE = 5, B_S = 7, B_P = 9, B_O = 11, B_NUM = 12 };
+// barriers: Q, K[2], V[2], KV-empty[2], S-full[2 tiles], P-full[2 tiles], O-final[2 tiles]
+enum { B_Q = 0, B_K = 1, B_V = 3, B_KVE = 5, B_S = 7, B_P = 9, B_OF = 11, B_NUM = 13 };
 
+constexpr int kFwdThreads = 12 * 32;  // TMA, MMA, 2 spare, 2 x 4 softmax warps
+
+// Two 128-row query tiles per CTA share every K/V tile (half the K/V smem traffic per
+// FLOP).  The tensor pipe alternates between them -- PV_0(j-1), S_0(j), PV_1(j-1), S_1(j)
+// -- so each softmax warpgroup works on its tile while the MMAs of the other run.
+// Because S_t(j) is issued after PV_t(j-1), the S_t(j) commit also retires PV_t(j-1):
+// the O rescale needs no extra barrier.
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     wf_block_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FwdArgs a) {
   using Cfg = FwdCfg<D>;
   constexpr int DP = Cfg::DP;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BAR + B_NUM * 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nqt = a.nq / WF_TILE;
-  // heavy tiles first: with zigzag units the later half of each unit sees more keys
-  const int qt = a.causal ? (nqt - 1 - blockIdx.x) : blockIdx.x;
+  const int npairs = (nqt + 1) >> 1;
+  // heavy pairs first: with zigzag units the later half of each unit sees more keys
+  const int pair = a.causal ? (npairs - 1 - blockIdx.x) : blockIdx.x;
   const int head = blockIdx.y;
-  const int q0 = qt * WF_TILE;
-  const int qpos0 = a.causal ? tile_gpos(a.qpos, q0) : q0;
+  const int q0 = pair * 2 * WF_TILE;
+  const bool hasB = q0 + WF_TILE < a.nq;
+  const int ntile = hasB ? 2 : 1;
+  const int qposA = a.causal ? tile_gpos(a.qpos, q0) : q0;
+  const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, q0 + WF_TILE) : q0 + WF_TILE;
   const int nkt = a.nk / WF_TILE;
   const bool has_state = a.o_in != nullptr;
+  // kind of (query tile t, key tile jt): 0 masked, 1 full, 2 diagonal
+  auto kind_of = [&](int t, int jt) -> int {
+    if (t == 1 && !hasB) return 0;
+    return tile_kind(a, t == 0 ? qposA : qposB, jt);
+  };
+  auto visible = [&](int jt) -> bool { return kind_of(0, jt) != 0 || kind_of(1, jt) != 0; };
 
   if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
     mbar_init(&bar[B_Q], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar[B_K + i], 1);
@@ -80,8 +100,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&bar[B_KVE + i], 1);
       mbar_init(&bar[B_S + i], 1);
       mbar_init(&bar[B_P + i], 128);
+      mbar_init(&bar[B_OF + i], 1);
     }
-    mbar_init(&bar[B_O], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -99,11 +119,14 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      mbar_arrive_expect_tx(&bar[B_Q], Cfg::TILE);
-      for (int p = 0; p < Cfg::NP; ++p) tma_load_3d(smem + Cfg::OFF_Q + p * Cfg::PANEL, &tmQ, &bar[B_Q], p * 64, head, q0);
+      mbar_arrive_expect_tx(&bar[B_Q], ntile * Cfg::TILE);
+      for (int t = 0; t < ntile; ++t)
+        for (int p = 0; p < Cfg::NP; ++p)
+          tma_load_3d(smem + Cfg::OFF_Q + t * Cfg::TILE + p * Cfg::PANEL, &tmQ, &bar[B_Q], p * 64, head,
+                      q0 + t * WF_TILE);
       int jj = 0;
       for (int jt = 0; jt < nkt; ++jt) {
-        if (tile_kind(a, qpos0, jt) == 0) continue;
+        if (!visible(jt)) continue;
         const int st = jj & 1;
         if (jj >= 2) mbar_wait(&bar[B_KVE + st], ((jj - 2) >> 1) & 1);
         uint8_t* sk = smem + Cfg::OFF_K + st * Cfg::TILE;
@@ -120,180 +143,188 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);  // Q (K-major) x K (K-major)
       constexpr uint32_t idO = idesc_bf16_f32(128, DP, 0, 1);   // P (TMEM) x V (MN-major)
-      const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q);
-      auto issue_pv = [&](int i) {
-        const int st = i & 1;
-        mbar_wait(&bar[B_P + st], (i >> 1) & 1);
-        mbar_wait(&bar[B_V + st], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(smem + Cfg::OFF_V + st * Cfg::TILE);
-#pragma unroll
-        for (int k = 0; k < WF_TILE / 16; ++k) {
-          const uint64_t bd = smem_desc_sw128(sV + k * 2048, Cfg::PANEL, 1024);
-          mma_ts(tbase + 256, tbase + st * 128 + k * 8, bd, idO, (i > 0 || has_state || k > 0) ? 1u : 0u);
-        }
-        mma_commit(&bar[B_KVE + st]);
-        mma_commit(&bar[B_O]);
-      };
-      mbar_wait(&bar[B_Q], 0);
-      tc_fence_after();
-      int jj = 0;
-      for (int jt = 0; jt < nkt; ++jt) {
-        if (tile_kind(a, qpos0, jt) == 0) continue;
-        const int st = jj & 1;
-        mbar_wait(&bar[B_K + st], (jj >> 1) & 1);
-        tc_fence_after();
+      auto issue_s = [&](int t, int j) {
+        const int st = j & 1;
+        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + t * Cfg::TILE);
         const uint32_t sK = smem_u32(smem + Cfg::OFF_K + st * Cfg::TILE);
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
           const int p = k >> 2, kk = k & 3;
-          const uint64_t ad = smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(sK + p * Cfg::PANEL + kk * 32, 16, 1024);
-          mma_ss(tbase + st * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+          mma_ss(tbase + t * 128, smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024),
+                 smem_desc_sw128(sK + p * Cfg::PANEL + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
         }
-        mma_commit(&bar[B_S + st]);
-        if (jj > 0) issue_pv(jj - 1);
-        ++jj;
+        mma_commit(&bar[B_S + t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(&bar[B_P + t], j & 1);
+        if (t == 0) mbar_wait(&bar[B_V + st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(smem + Cfg::OFF_V + st * Cfg::TILE);
+#pragma unroll
+        for (int k = 0; k < WF_TILE / 16; ++k)
+          mma_ts(tbase + 256 + t * 128, tbase + t * 128 + k * 8, smem_desc_sw128(sV + k * 2048, Cfg::PANEL, 1024),
+                 idO, (j > 0 || has_state || k > 0) ? 1u : 0u);
+      };
+      int nvis = 0;
+      for (int jt = 0; jt < nkt; ++jt) nvis += visible(jt);
+      mbar_wait(&bar[B_Q], 0);
+      for (int j = 0; j < nvis; ++j) {
+        const int st = j & 1;
+        mbar_wait(&bar[B_K + st], (j >> 1) & 1);
+        tc_fence_after();
+        for (int t = 0; t < ntile; ++t) {
+          if (j > 0) issue_pv(t, j - 1);
+          issue_s(t, j);
+        }
+        if (j > 0) mma_commit(&bar[B_KVE + ((j - 1) & 1)]);
       }
-      if (jj > 0) issue_pv(jj - 1);
+      if (nvis > 0) {
+        for (int t = 0; t < ntile; ++t) {
+          issue_pv(t, nvis - 1);
+          mma_commit(&bar[B_OF + t]);
+        }
+        mma_commit(&bar[B_KVE + ((nvis - 1) & 1)]);
+      } else {
+        for (int t = 0; t < ntile; ++t) mma_commit(&bar[B_OF + t]);
+      }
     }
-  } else {
-    // ------------------------------------------------------------ softmax + epilogue
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue (tile t)
+    const int t = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
-    const uint32_t tl = tbase + (static_cast<uint32_t>(wq * 32) << 16);
-    const int grow = q0 + row;
-    const size_t orow = (static_cast<size_t>(grow) * a.heads + head) * D;
-    float m = -INFINITY, l = 0.f;
-    if (has_state) {
-      const float ls = a.lse_in[stat_index(head, grow, a.heads, a.lse_blk)];
-      m = ls * kLog2e;
-      l = (ls == -INFINITY) ? 0.f : 1.f;
+    if (t == 1 && !hasB) {
+      // no second tile in this CTA
+    } else {
+      const uint32_t tl = tbase + (static_cast<uint32_t>(wq * 32) << 16);
+      const uint32_t cS = t * 128, cO = 256 + t * 128;
+      const int grow = q0 + t * WF_TILE + row;
+      const size_t orow = (static_cast<size_t>(grow) * a.heads + head) * D;
+      float m = -INFINITY, l = 0.f;
+      if (has_state) {
+        const float ls = a.lse_in[stat_index(head, grow, a.heads, a.lse_blk)];
+        m = ls * kLog2e;
+        l = (ls == -INFINITY) ? 0.f : 1.f;
+#pragma unroll
+        for (int c = 0; c < DP / 16; ++c) {
+          uint32_t r[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = c * 16 + i;
+            r[i] = __float_as_uint(col < D ? a.o_in[orow + col] : 0.f);
+          }
+          tmem_st16(tl + cO + c * 16, r);
+        }
+        tmem_wait_st();
+      }
+      int j = 0;
+      for (int jt = 0; jt < nkt; ++jt) {
+        if (!visible(jt)) continue;
+        const int kind = kind_of(t, jt);
+        mbar_wait(&bar[B_S + t], j & 1);
+        tc_fence_after();
+        float s[128];
+        {
+          uint32_t r0[32], r1[32], r2[32], r3[32];
+          tmem_ld32(tl + cS + 0, r0);
+          tmem_ld32(tl + cS + 32, r1);
+          tmem_ld32(tl + cS + 64, r2);
+          tmem_ld32(tl + cS + 96, r3);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            s[i] = __uint_as_float(r0[i]);
+            s[32 + i] = __uint_as_float(r1[i]);
+            s[64 + i] = __uint_as_float(r2[i]);
+            s[96 + i] = __uint_as_float(r3[i]);
+          }
+        }
+        if (kind != 1) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (kind == 0 || c > row) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        const float mcand = mx * a.scale_log2;
+        const bool need = mcand > m + 8.0f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float mnew = fmaxf(m, mcand);
+          const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mnew);
+          if (j > 0 || has_state) {
+            // PV_t(j-1) retired with the S_t(j) commit (issued before it)
+#pragma unroll
+            for (int c = 0; c < DP / 16; ++c) {
+              uint32_t r[16];
+              tmem_ld16(tl + cO + c * 16, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tmem_st16(tl + cO + c * 16, r);
+            }
+          }
+          l *= alpha;
+          m = mnew;
+        }
+        const float mm = (m == -INFINITY) ? 0.f : m;
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = fast_exp2(fmaf(s[c * 32 + 2 * i], a.scale_log2, -mm));
+            const float p1 = fast_exp2(fmaf(s[c * 32 + 2 * i + 1], a.scale_log2, -mm));
+            rs += p0 + p1;
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+          tmem_st16(tl + cS + c * 16, pk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bar[B_P + t]);
+        l += rs;
+        ++j;
+      }
+      // epilogue
+      mbar_wait(&bar[B_OF + t], 0);
+      tc_fence_after();
+      const bool have_o = j > 0 || has_state;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      a.lse_out[stat_index(head, grow, a.heads, a.lse_blk)] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
 #pragma unroll
       for (int c = 0; c < DP / 16; ++c) {
         uint32_t r[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c * 16 + i;
-          r[i] = __float_as_uint(col < D ? a.o_in[orow + col] : 0.f);
+        if (have_o) {
+          tmem_ld16(tl + cO + c * 16, r);
+          tmem_wait_ld();
         }
-        tmem_st16(tl + 256 + c * 16, r);
-      }
-      tmem_wait_st();
-    }
-    int jj = 0;
-    for (int jt = 0; jt < nkt; ++jt) {
-      const int kind = tile_kind(a, qpos0, jt);
-      if (kind == 0) continue;
-      const int st = jj & 1;
-      mbar_wait(&bar[B_S + st], (jj >> 1) & 1);
-      tc_fence_after();
-      float s[128];
-      {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        tmem_ld32(tl + st * 128 + 0, r0);
-        tmem_ld32(tl + st * 128 + 32, r1);
-        tmem_ld32(tl + st * 128 + 64, r2);
-        tmem_ld32(tl + st * 128 + 96, r3);
-        tmem_wait_ld();
+        float v[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = __uint_as_float(r0[i]);
-          s[32 + i] = __uint_as_float(r1[i]);
-          s[64 + i] = __uint_as_float(r2[i]);
-          s[96 + i] = __uint_as_float(r3[i]);
-        }
-      }
-      if (kind == 2) {
+        for (int i = 0; i < 16; ++i) v[i] = have_o ? __uint_as_float(r[i]) * inv : 0.f;
+        if (c * 16 + 16 <= D) {
+          if (a.o_out_f32) {
+            float4* dst = reinterpret_cast<float4*>(a.o_out_f32 + orow + c * 16);
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > row) s[c] = -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-      const float mcand = mx * a.scale_log2;
-      const bool need = mcand > m + 8.0f;
-      if (__any_sync(0xffffffffu, need)) {
-        const float mnew = fmaxf(m, mcand);
-        const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mnew);
-        if (jj > 0 || has_state) {
-          if (jj > 0) {
-            mbar_wait(&bar[B_O], (jj - 1) & 1);
-            tc_fence_after();
+            for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           }
+          if (a.o_out_bf16) {
+            uint4* dst = reinterpret_cast<uint4*>(a.o_out_bf16 + orow + c * 16);
 #pragma unroll
-          for (int c = 0; c < DP / 16; ++c) {
-            uint32_t r[16];
-            tmem_ld16(tl + 256 + c * 16, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st16(tl + 256 + c * 16, r);
+            for (int i = 0; i < 2; ++i)
+              dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                  pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
           }
-        }
-        l *= alpha;
-        m = mnew;
-      }
-      const float mm = (m == -INFINITY) ? 0.f : m;
-      float rs = 0.f;
+        } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float p0 = fast_exp2(fmaf(s[c * 32 + 2 * i], a.scale_log2, -mm));
-          const float p1 = fast_exp2(fmaf(s[c * 32 + 2 * i + 1], a.scale_log2, -mm));
-          rs += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(tl + st * 128 + c * 16, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bar[B_P + st]);
-      l += rs;
-      ++jj;
-    }
-    // epilogue
-    const int ntiles = jj;
-    if (ntiles > 0) {
-      mbar_wait(&bar[B_O], (ntiles - 1) & 1);
-      tc_fence_after();
-    }
-    const bool have_o = ntiles > 0 || has_state;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    a.lse_out[stat_index(head, grow, a.heads, a.lse_blk)] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
-#pragma unroll
-    for (int c = 0; c < DP / 16; ++c) {
-      uint32_t r[16];
-      if (have_o) {
-        tmem_ld16(tl + 256 + c * 16, r);
-        tmem_wait_ld();
-      }
-      float v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = have_o ? __uint_as_float(r[i]) * inv : 0.f;
-      if (c * 16 + 16 <= D) {
-        if (a.o_out_f32) {
-          float4* dst = reinterpret_cast<float4*>(a.o_out_f32 + orow + c * 16);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-        if (a.o_out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(a.o_out_bf16 + orow + c * 16);
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c * 16 + i;
-          if (col < D) {
-            if (a.o_out_f32) a.o_out_f32[orow + col] = v[i];
-            if (a.o_out_bf16) a.o_out_bf16[orow + col] = __float2bfloat16_rn(v[i]);
+          for (int i = 0; i < 16; ++i) {
+            const int col = c * 16 + i;
+            if (col < D) {
+              if (a.o_out_f32) a.o_out_f32[orow + col] = v[i];
+              if (a.o_out_bf16) a.o_out_bf16[orow + col] = __float2bfloat16_rn(v[i]);
+            }
           }
         }
       }
@@ -314,8 +345,8 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(a.nq / WF_TILE, a.heads);
-  wf_block_fwd_kernel<D><<<grid, 192, Cfg::SMEM, s>>>(tq, tk, tv, a);
+  dim3 grid((a.nq / WF_TILE + 1) / 2, a.heads);
+  wf_block_fwd_kernel<D><<<grid, kFwdThreads, Cfg::SMEM, s>>>(tq, tk, tv, a);
   return cudaGetLastError();
 }
 

@@ -32,26 +32,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)  // suspend up to ~1 ms per try
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-// Spin on an mbarrier phase.  A wait longer than ~20 s is a protocol bug: trap so the
-// launch fails loudly instead of hanging the GPU.
+// Wait for an mbarrier phase.  try_wait suspends the thread in hardware until the phase
+// completes (or the hint expires), so waiting warps do not steal issue slots.  A wait
+// that outlives ~2^22 retries (seconds) is a protocol bug: trap instead of hanging.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+    if (++n > (1u << 22)) __trap();
   }
 }
 

@@ -1,0 +1,146 @@
+"""Multi-process tests of the N > 1 path.
+
+* CPU (gloo, world_size 2): the host side of a real multi-rank job -- rank 0 creates the
+  NCCL id through the C ABI, torch.distributed broadcasts it, every rank computes its own
+  CommTrace (wf_plan_trace, rank-filtered) and the union over ranks equals the oracle's
+  literal schedule simulation.
+* GPU (NCCL, one process per GPU; run under `gpurun --gpus 2` or more): the real
+  wf_init / wf_attn_fwd / wf_attn_bwd over NVLink, values against the fp64 dense oracle
+  and each rank's recorded trace against the oracle's records sent by that rank.
+"""
+import os
+import socket
+from collections import Counter
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.schedule import simulate_backward, simulate_forward
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_events(P, C, N, h, d, causal):
+    _, _, ef, _ = simulate_forward(N, None, None, P, C, causal, compute=False, heads=h, head_dim=d)
+    _, _, _, eb = simulate_backward(N, None, None, None, None, None, P, C, causal, compute=False, heads=h, head_dim=d)
+    return [(e.pas, e.kind, e.step, e.src, e.dst, e.block, e.nbytes) for e in ef + eb]
+
+
+def _cpu_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes
+        from paper_2407_00611_b200._lib import WfUid, lib
+        import paper_2407_00611_b200 as wf
+        uid = WfUid()
+        if rank == 0:
+            assert lib().wf_get_uid(ctypes.byref(uid)) == 0
+        t = torch.tensor(list(bytes(uid.bytes)), dtype=torch.uint8)
+        dist.broadcast(t, src=0)
+        got = bytes(t.tolist())
+        allu = [None] * world
+        dist.all_gather_object(allu, got)
+        traces = {}
+        for P, C in ((2, 2), (4, 2), (8, 2), (8, 4), (4, 1)):
+            # the P ranks of the simulated job are split across the world processes
+            mine = []
+            for r in range(rank, P, world):
+                mine += wf.plan_trace(P, C, 512 * P, 2, 64, rank=r)
+            parts = [None] * world
+            dist.all_gather_object(parts, mine)
+            traces[(P, C)] = [e for p in parts for e in p]
+        if rank == 0:
+            q.put((allu, traces))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_host_path():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allu, traces = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(set(allu)) == 1 and any(allu[0])
+    for (P, C), tr in traces.items():
+        assert Counter(tr) == Counter(_oracle_events(P, C, 512 * P, 2, 64, False)), (P, C)
+
+
+# ---------------------------------------------------------------------- GPU (NCCL)
+def _gpu_worker(rank, world, port, C, N, causal, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import paper_2407_00611_b200 as wf
+        from wf_inputs import make_qkv_do
+        from oracle.sharding import unit_positions
+        h, d = 2, 128
+        qg, kg, vg, dog = make_qkv_do(N, h, d, seed=21, peaky=True)
+        idx = torch.from_numpy(unit_positions(rank, world, N, causal))
+        qs, ks, vs, dos = (t[idx].contiguous().cuda() for t in (qg, kg, vg, dog))
+        ctx = wf.Context(world, C, rank=rank)
+        o, lse = ctx.fwd(qs, ks, vs, N, causal)
+        dq, dk, dv = ctx.bwd(dos, qs, ks, vs, o, lse, N, causal)
+        torch.cuda.synchronize()
+        tr = ctx.trace()
+        ctx.close()
+        res = [x.cpu() for x in (o, lse, dq, dk, dv)]
+        allres = [None] * world
+        dist.all_gather_object(allres, (res, tr))
+        if rank == 0:
+            q.put(allres)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.parametrize("C", [1, 2])
+@pytest.mark.parametrize("causal", [True, False])
+def test_nccl_real_path(C, causal):
+    from oracle.dense import attention_bwd
+    from oracle.sharding import unit_positions
+    from wf_inputs import make_qkv_do, to_f64
+    world = min(torch.cuda.device_count(), 4)
+    if world % C:
+        pytest.skip("C must divide the GPU count")
+    N = 512 * world
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, C, N, causal, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allres = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    h, d = 2, 128
+    qg, kg, vg, dog = make_qkv_do(N, h, d, seed=21, peaky=True)
+    dq_r, dk_r, dv_r, o_r, l_r = attention_bwd(to_f64(qg), to_f64(kg), to_f64(vg), to_f64(dog), causal=causal)
+    trace = []
+    for r, (res, tr) in enumerate(allres):
+        pos = unit_positions(r, world, N, causal)
+        o, lse, dq, dk, dv = (x.double().numpy() for x in res)
+        assert np.abs(o - o_r[pos]).max() <= 2e-2
+        assert np.abs(lse - l_r[:, pos]).max() <= 1e-2
+        for g, ref in ((dq, dq_r), (dk, dk_r), (dv, dv_r)):
+            assert np.abs(g - ref[pos]).max() / np.abs(ref).max() <= 2e-2
+        assert all(e[3] == r for e in tr)
+        trace += tr
+    assert Counter(trace) == Counter(_oracle_events(world, C, N, h, d, causal))
