@@ -228,6 +228,23 @@ def main():
     ff, fb = flops(N, heads, hd, causal)
     total_tflops = (ff + fb) * args.steps / (ms / 1e3) / 1e12
 
+    # exposed communication: same steps with every inter-rank transfer skipped
+    exposed = None
+    if world > 1:
+        ctx.set_debug(1)
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        for _ in range(args.steps):
+            step()
+        n1.record(stream)
+        barrier()
+        ctx.set_debug(0)
+        tn = torch.tensor([n0.elapsed_time(n1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+        t_nocomm = float(tn.item())
+        exposed = {"frac": max(0.0, (ms - t_nocomm) / ms), "ms_per_step_no_transfer": t_nocomm / args.steps}
+
     # roofline of the dominant kernel (the block backward: 5 of the 7 GEMM-equivalents)
     peaks = load_peaks()
     peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
@@ -298,6 +315,7 @@ def main():
                          "unit": "TFLOP/s", "frac": (achieved_b / peak) if achieved_b else None, "traffic": None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                          "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
+            "exposed_comm": exposed,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

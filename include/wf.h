@@ -128,6 +128,13 @@ int64_t wf_kernel_launches(const wf_ctx* ctx);
 wf_status wf_set_profiling(wf_ctx* ctx, int on);
 wf_status wf_kernel_times(wf_ctx* ctx, double out[4]);
 
+/* Measurement aid (bench): flags = WF_DEBUG_NO_TRANSFER skips every inter-rank transfer
+ * (the kernels run on whatever the receive buffers hold, the trace is still recorded), so
+ * T(no transfer) / T gives the exposed-communication fraction with identical kernels.
+ * Results are garbage in that mode. */
+#define WF_DEBUG_NO_TRANSFER 1
+wf_status wf_set_debug(wf_ctx* ctx, int flags);
+
 /* Last error text of ctx (or of the last context-less call when ctx is NULL). */
 const char* wf_last_error(const wf_ctx* ctx);
 

@@ -90,6 +90,7 @@ struct wf_ctx {
   std::vector<wf_event> trace_fwd, trace_bwd;
   int64_t launches = 0;
   std::string err;
+  int debug = 0;
   // kernel timing (bench)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_fwd, ev_bwd;
@@ -267,6 +268,7 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
     trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
   }
   if (ctx->dry) return WF_OK;
+  if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
   if (ctx->emulated) {
     for (const Xfer& x : xs)
       for (const Seg& s : x.segs)
@@ -987,6 +989,12 @@ wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges
 }
 
 int64_t wf_kernel_launches(const wf_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+wf_status wf_set_debug(wf_ctx* ctx, int flags) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  ctx->debug = flags;
+  return WF_OK;
+}
 
 wf_status wf_set_profiling(wf_ctx* ctx, int on) {
   if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");

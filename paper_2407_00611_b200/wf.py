@@ -150,6 +150,10 @@ class Context:
         _check(lib().wf_get_trace(self.h, buf, n.value, ctypes.byref(n)), self.h)
         return _events(buf, n.value)
 
+    def set_debug(self, flags):
+        """flags: 1 = skip every inter-rank transfer (timing of exposed communication only)."""
+        _check(lib().wf_set_debug(self.h, int(flags)), self.h)
+
     def set_profiling(self, on=True):
         _check(lib().wf_set_profiling(self.h, int(on)), self.h)
 
