@@ -219,6 +219,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches() - launches0
     fwd_ms, bwd_ms, nf, nb = ctx.kernel_times()
+    phase_ms = {k: v / args.steps for k, v in ctx.phase_times().items()}
     ctx.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -316,6 +317,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                          "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
             "exposed_comm": exposed,
+            "phase_ms_per_step": phase_ms,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -127,6 +127,9 @@ int64_t wf_kernel_launches(const wf_ctx* ctx);
  * enabled (out[0] fwd ms, out[1] bwd ms, out[2] fwd launches, out[3] bwd launches). */
 wf_status wf_set_profiling(wf_ctx* ctx, int on);
 wf_status wf_kernel_times(wf_ctx* ctx, double out[4]);
+/* With profiling on: device milliseconds spent in each message phase since the last call,
+ * summed by WF_KIND_* (ms_by_kind[0..n)), measured by events on the phase's stream. */
+wf_status wf_phase_times(wf_ctx* ctx, double* ms_by_kind, int n);
 
 /* Measurement aid (bench): flags = WF_DEBUG_NO_TRANSFER skips every inter-rank transfer
  * (the kernels run on whatever the receive buffers hold, the trace is still recorded), so

@@ -42,6 +42,7 @@ _SIGS = {
     "wf_kernel_launches": (c_i64, [c_p]),
     "wf_set_profiling": (c_int, [c_p, c_int]),
     "wf_set_debug": (c_int, [c_p, c_int]),
+    "wf_phase_times": (c_int, [c_p, ctypes.POINTER(ctypes.c_double), c_int]),
     "wf_kernel_times": (c_int, [c_p, ctypes.POINTER(ctypes.c_double)]),
     "wf_last_error": (ctypes.c_char_p, [c_p]),
     "wf_finalize": (c_int, [c_p]),

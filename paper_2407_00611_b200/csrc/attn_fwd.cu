@@ -23,6 +23,9 @@ using namespace sm100;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef WF_POLY_EVERY
+#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU)
+#endif
 constexpr float kLn2 = 0.6931471805599453f;
 
 __device__ __forceinline__ int tile_gpos(const PosTable& t, int row0) {
@@ -275,8 +278,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float p0 = fast_exp2(fmaf(s[c * 32 + 2 * i], a.scale_log2, -mm));
-            const float p1 = fast_exp2(fmaf(s[c * 32 + 2 * i + 1], a.scale_log2, -mm));
+            const float x0 = fmaf(s[c * 32 + 2 * i], a.scale_log2, -mm);
+            const float x1 = fmaf(s[c * 32 + 2 * i + 1], a.scale_log2, -mm);
+#if WF_POLY_EVERY > 0
+            const bool poly = ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
+            const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+            const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+#else
+            const float p0 = fast_exp2(x0);
+            const float p1 = fast_exp2(x1);
+#endif
             rs += p0 + p1;
             pk[i] = pack_bf16x2(p0, p1);
           }

@@ -95,3 +95,15 @@ cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* 
                         cudaStream_t s);
 cudaError_t launch_sum(const SumArgs& a, cudaStream_t s);
 }  // namespace wf
+
+#define WF_MAX_SIG 64
+namespace wf {
+// A batch of flag updates (signal) or flag conditions (wait): dst[i] is a flag address,
+// val[i] the count to publish / to wait for.
+struct SigArgs {
+  int n;
+  uint32_t* dst[WF_MAX_SIG];
+  uint32_t val[WF_MAX_SIG];
+};
+cudaError_t launch_signal_wait(const SigArgs& sig, const SigArgs& wait, cudaStream_t s);
+}  // namespace wf

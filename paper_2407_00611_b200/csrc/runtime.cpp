@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -67,7 +68,11 @@ struct Seg {
 struct Xfer {
   int pass, kind, step, src, dst, block;
   std::vector<Seg> segs;
+  bool pull = false;  // peer-memory transport: the consumer kernel reads the source in place
 };
+
+constexpr size_t kFlagBytes = 4096;  // flag block at the start of every rank's workspace
+constexpr int kMaxRanks = 64;
 
 }  // namespace
 }  // namespace wf
@@ -91,9 +96,19 @@ struct wf_ctx {
   int64_t launches = 0;
   std::string err;
   int debug = 0;
+  // peer-memory transport (real mode, P > 1): CUDA IPC mapped workspaces + flag signalling
+  bool ipc = false;
+  std::vector<char*> peer_base;
+  std::vector<RankBufs> rbp;       // my layout translated into each rank's address space
+  uint32_t sent[2][kMaxRanks] = {}, rcvd[2][kMaxRanks] = {};
+  uint32_t acks_sent[kMaxRanks] = {}, ack_base[kMaxRanks] = {};  // monotonic across calls
+  uint32_t epoch = 0;
+  std::vector<cudaEvent_t> ev_step;
+  cudaEvent_t ev_c = nullptr;
   // kernel timing (bench)
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_fwd, ev_bwd;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_phase;  // (kind, events)
   std::vector<cudaEvent_t> ev_pool;
 };
 
@@ -176,6 +191,63 @@ PosTable units_table(const Geo& g, int u0, int count) {
   return t;
 }
 
+// ------------------------------------------------------------------ peer memory
+// Exchange CUDA IPC handles of every rank's workspace (an NCCL all-gather of the 64-byte
+// handles), map the peers' workspaces, and translate my buffer layout into each rank's
+// address space (all ranks carve identical layouts).
+RankBufs translate(const RankBufs& b, const char* from, const char* to) {
+  RankBufs t = b;
+  char** f = reinterpret_cast<char**>(&t);
+  for (size_t i = 0; i < sizeof(RankBufs) / sizeof(char*); ++i)
+    if (f[i]) f[i] = const_cast<char*>(to) + (f[i] - from);
+  return t;
+}
+
+wf_status exchange_ipc(wf_ctx* ctx) {
+  const int P = ctx->plan.P, me = ctx->rank;
+  for (size_t r = 0; r < ctx->peer_base.size(); ++r)
+    if (static_cast<int>(r) != me && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->ws));
+  void* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, static_cast<size_t>(P) * sizeof(h)));
+  CK(cudaMemcpy(static_cast<char*>(dbuf) + me * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCK(ncclAllGather(static_cast<char*>(dbuf) + me * sizeof(h), dbuf, sizeof(h), ncclInt8, ctx->comm, ctx->comm_stream));
+  CK(cudaStreamSynchronize(ctx->comm_stream));
+  std::vector<cudaIpcMemHandle_t> hs(P);
+  CK(cudaMemcpy(hs.data(), dbuf, P * sizeof(h), cudaMemcpyDeviceToHost));
+  CK(cudaFree(dbuf));
+  ctx->peer_base.assign(P, nullptr);
+  ctx->rbp.assign(P, RankBufs{});
+  for (int r = 0; r < P; ++r) {
+    if (r == me) {
+      ctx->peer_base[r] = static_cast<char*>(ctx->ws);
+    } else {
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess));
+      ctx->peer_base[r] = static_cast<char*>(p);
+    }
+    ctx->rbp[r] = translate(ctx->rb[0], static_cast<char*>(ctx->ws), ctx->peer_base[r]);
+  }
+  // fresh flag blocks everywhere: no stale counts
+  std::memset(ctx->sent, 0, sizeof(ctx->sent));
+  std::memset(ctx->rcvd, 0, sizeof(ctx->rcvd));
+  std::memset(ctx->acks_sent, 0, sizeof(ctx->acks_sent));
+  std::memset(ctx->ack_base, 0, sizeof(ctx->ack_base));
+  ctx->epoch = 0;
+  // every rank has zeroed its flags before anyone signals (the all-gather above ordered
+  // the memsets; this second one orders the mappings)
+  int32_t* scratch = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->ws) + kFlagBytes - 64);
+  NCK(ncclAllReduce(scratch, scratch, 1, ncclInt32, ncclSum, ctx->comm, ctx->comm_stream));
+  CK(cudaStreamSynchronize(ctx->comm_stream));
+  return WF_OK;
+}
+
+// flag addresses: data[chan][src] at word chan*64 + src, ack[src] at 128 + src, bar[src] at 192 + src
+uint32_t* flag_of(wf_ctx* ctx, int owner, int word) {
+  return reinterpret_cast<uint32_t*>(ctx->peer_base[owner]) + word;
+}
+
 // ------------------------------------------------------------------ workspace
 wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   if (ctx->dry) {
@@ -186,6 +258,9 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   if (ctx->ws && std::equal(key, key + 4, ctx->ws_key)) return WF_OK;
   if (ctx->ws) {
     CK(cudaDeviceSynchronize());
+    for (size_t r = 0; r < ctx->peer_base.size(); ++r)
+      if (static_cast<int>(r) != ctx->rank && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
+    ctx->peer_base.clear();
     CK(cudaFree(ctx->ws));
     ctx->ws = nullptr;
   }
@@ -241,11 +316,13 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
       add(&b.rev_v, static_cast<int64_t>(g.T) * n * E * 4);
     }
   }
-  size_t total = 0;
+  size_t total = kFlagBytes;
   for (auto& it : items) total += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
   void* base = nullptr;
   CK(cudaMalloc(&base, total));
-  size_t off = 0;
+  CK(cudaMemset(base, 0, kFlagBytes));
+  CK(cudaDeviceSynchronize());
+  size_t off = kFlagBytes;
   for (auto& it : items) {
     *it.first = static_cast<char*>(base) + off;
     off += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
@@ -254,10 +331,19 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   ctx->ws_bytes = total;
   std::copy(key, key + 4, ctx->ws_key);
   ctx->rb = rb;
+  if (ctx->ipc) WCK(exchange_ipc(ctx));
   return WF_OK;
 }
 
-RankBufs& B(wf_ctx* ctx, int r) { return ctx->rb[ctx->emulated || ctx->dry ? r : 0]; }
+RankBufs& B(wf_ctx* ctx, int r) {
+  if (ctx->ipc && !ctx->dry) return ctx->rbp[r];
+  return ctx->rb[ctx->emulated || ctx->dry ? r : 0];
+}
+// a rank's workspace buffer is addressable here: own/emulated ranks, or any rank with IPC
+bool addressable(const wf_ctx* ctx, int r) { return local(ctx, r) || (ctx->ipc && !ctx->dry); }
+
+cudaEvent_t pool_event(wf_ctx* ctx);
+cudaEvent_t prof_begin(wf_ctx* ctx, cudaStream_t st);
 
 // ------------------------------------------------------------------ transport
 wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& trace, cudaStream_t st) {
@@ -276,6 +362,49 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
     return WF_OK;
   }
   const int me = ctx->rank;
+  if (ctx->ipc) {
+    const int ch = st == ctx->comm_stream ? 1 : 0;
+    cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
+    for (const Xfer& x : xs) {
+      if (x.src != me || x.pull) continue;
+      for (const Seg& sg : x.segs)
+        if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
+    }
+    SigArgs sig{}, wt{};
+    bool dst_done[kMaxRanks] = {}, src_done[kMaxRanks] = {};
+    for (const Xfer& x : xs) {
+      if (x.src == me && x.dst != me && !dst_done[x.dst]) {
+        dst_done[x.dst] = true;
+        sig.dst[sig.n] = flag_of(ctx, x.dst, ch * 64 + me);
+        sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
+      }
+      if (x.dst == me && x.src != me && !src_done[x.src]) {
+        src_done[x.src] = true;
+        wt.dst[wt.n] = flag_of(ctx, me, ch * 64 + x.src);
+        wt.val[wt.n++] = ++ctx->rcvd[ch][x.src];
+      }
+    }
+    CK(launch_signal_wait(sig, wt, st));
+    if (pe0) {
+      cudaEvent_t e1 = pool_event(ctx);
+      cudaEventRecord(e1, st);
+      ctx->ev_phase.push_back({xs[0].kind, {pe0, e1}});
+    }
+    return WF_OK;
+  }
+  cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
+  struct PhaseEnd {
+    wf_ctx* c;
+    cudaStream_t s;
+    cudaEvent_t e0;
+    int kind;
+    ~PhaseEnd() {
+      if (!e0) return;
+      cudaEvent_t e1 = pool_event(c);
+      cudaEventRecord(e1, s);
+      c->ev_phase.push_back({kind, {e0, e1}});
+    }
+  } pend{ctx, st, pe0, xs.empty() ? 0 : xs[0].kind};
   bool any = false;
   for (const Xfer& x : xs) any = any || ((x.src == me) != (x.dst == me));
   if (any) NCK(ncclGroupStart());
@@ -331,6 +460,61 @@ wf_status kcheck(wf_ctx* ctx, cudaError_t e, const char* what) {
   return WF_OK;
 }
 
+// ------------------------------------------------------------------ peer-memory sync helpers
+// Per-call barrier of all ranks: no peer writes into my workspace before I have finished
+// reading what the previous call left there (stream order puts this after my previous work).
+wf_status ipc_barrier(wf_ctx* ctx, cudaStream_t st) {
+  if (!ctx->ipc || ctx->dry || (ctx->debug & WF_DEBUG_NO_TRANSFER)) return WF_OK;
+  const int P = ctx->plan.P, me = ctx->rank;
+  ++ctx->epoch;
+  SigArgs sig{}, wt{};
+  for (int r = 0; r < P; ++r) {
+    if (r == me) continue;
+    sig.dst[sig.n] = flag_of(ctx, r, 192 + me);
+    sig.val[sig.n++] = ctx->epoch;
+    wt.dst[wt.n] = flag_of(ctx, me, 192 + r);
+    wt.val[wt.n++] = ctx->epoch;
+  }
+  CK(launch_signal_wait(sig, wt, st));
+  return WF_OK;
+}
+// Tell `to` that I finished reading the ring slot it fills (one more released slot).
+wf_status ipc_ack(wf_ctx* ctx, int to, cudaStream_t st) {
+  if (!ctx->ipc || ctx->dry || (ctx->debug & WF_DEBUG_NO_TRANSFER) || to == ctx->rank) return WF_OK;
+  SigArgs sig{}, wt{};
+  sig.dst[0] = flag_of(ctx, to, 128 + ctx->rank);
+  sig.val[0] = ++ctx->acks_sent[to];
+  sig.n = 1;
+  CK(launch_signal_wait(sig, wt, st));
+  return WF_OK;
+}
+// Wait until `from` has released `count` slots in this ring loop (ack_base counts the
+// releases of earlier loops; every loop releases R - 1 slots).
+wf_status ipc_wait_ack(wf_ctx* ctx, int from, uint32_t count, cudaStream_t st) {
+  if (!ctx->ipc || ctx->dry || (ctx->debug & WF_DEBUG_NO_TRANSFER) || from == ctx->rank || count == 0) return WF_OK;
+  SigArgs sig{}, wt{};
+  wt.dst[0] = flag_of(ctx, ctx->rank, 128 + from);
+  wt.val[0] = ctx->ack_base[from] + count;
+  wt.n = 1;
+  CK(launch_signal_wait(sig, wt, st));
+  return WF_OK;
+}
+cudaEvent_t step_event(wf_ctx* ctx, int i) {
+  while (static_cast<int>(ctx->ev_step.size()) <= i) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ctx->ev_step.push_back(e);
+  }
+  return ctx->ev_step[i];
+}
+// join the comm stream back into the caller's stream
+wf_status join_comm(wf_ctx* ctx, cudaStream_t st) {
+  if (ctx->dry || ctx->emulated) return WF_OK;
+  CK(cudaEventRecord(ctx->ev_c, ctx->comm_stream));
+  CK(cudaStreamWaitEvent(st, ctx->ev_c, 0));
+  return WF_OK;
+}
+
 // ------------------------------------------------------------------ forward
 wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const bf16* V, bf16* O, float* LSE,
                   cudaStream_t st) {
@@ -342,9 +526,10 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   auto Vin = [&](int r) { return local(ctx, r) ? V + (ctx->emulated ? r * n * E : 0) : nullptr; };
   auto Oout = [&](int r) { return local(ctx, r) ? O + (ctx->emulated ? r * n * E : 0) : nullptr; };
   auto Lout = [&](int r) { return local(ctx, r) ? LSE + (ctx->emulated ? r * n * h : 0) : nullptr; };
-  auto lp = [&](int r, auto* p) { return local(ctx, r) ? p : decltype(p)(nullptr); };
+  auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_fwd;
   tr.clear();
+  WCK(ipc_barrier(ctx, st));
 
   // Team tensors (C = 1: the caller's shard itself).
   auto qteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).qt) : Qin(r); };
@@ -463,7 +648,14 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         x.segs.push_back({slot_v(r, s), lp(dst, B(ctx, dst).rv[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
         xs.push_back(x);
       }
-      if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
+      if (overlap && ctx->ipc) {
+        // Alg. 1 l.8 with peer copies: the comm stream pushes block s into next's other
+        // slot as soon as next has released it (its step s-1), independent of my compute.
+        if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+        WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
+        WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
+        CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
+      } else if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
         CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
         WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
         CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
@@ -472,7 +664,10 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
     for (int r = 0; r < P; ++r)
       if (local(ctx, r)) WCK(compute(r, s));
     if (s < R - 1) {
-      if (overlap) {
+      if (overlap && ctx->ipc) {
+        WCK(ipc_ack(ctx, pl.last[ctx->rank], st));  // my slot s is free again
+        CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
+      } else if (overlap) {
         CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
         CK(cudaEventRecord(ctx->ev_a, st));
       } else {
@@ -480,6 +675,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       }
     }
   }
+  if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
 
   // Alg. 1 l.11: ReduceScatter_combine -- partial rows to their owner, LSE-merge there.
   if (C > 1) {
@@ -489,10 +685,12 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       for (int p = t * C; p < t * C + C; ++p) {
         if (p == r) continue;
         const int jp = p - t * C;
-        Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}};
+        // peer-memory transport: the owner's merge kernel reads the partial in place
+        // (fused reduce-scatter); otherwise it is copied into the owner's slot first.
+        Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}, ctx->ipc};
         x.segs.push_back({at(lp(r, B(ctx, r).o_state), jp * n * E), at(lp(p, B(ctx, p).rs_o), j * n * E), n * E * 4});
         xs.push_back(x);
-        Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}};
+        Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}, ctx->ipc};
         y.segs.push_back({at(lp(r, B(ctx, r).lse_state), jp * h * n), at(lp(p, B(ctx, p).rs_lse), j * h * n), h * n * 4});
         xs.push_back(y);
       }
@@ -507,9 +705,18 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       m.heads = g.h;
       m.D = g.d;
       m.nparts = C;
+      const int t0 = (r / C) * C;
       for (int i = 0; i < C; ++i) {
-        m.o[i] = i == j ? b.o_state + i * n * E : b.rs_o + i * n * E;
-        m.lse[i] = i == j ? b.lse_state + i * h * n : b.rs_lse + i * h * n;
+        if (i == j) {
+          m.o[i] = b.o_state + i * n * E;
+          m.lse[i] = b.lse_state + i * h * n;
+        } else if (ctx->ipc) {  // member i's partial of my rows, read over NVLink
+          m.o[i] = B(ctx, t0 + i).o_state + j * n * E;
+          m.lse[i] = B(ctx, t0 + i).lse_state + j * h * n;
+        } else {
+          m.o[i] = b.rs_o + i * n * E;
+          m.lse[i] = b.rs_lse + i * h * n;
+        }
         m.lse_stride[i] = n;
       }
       m.out = Oout(r);
@@ -517,7 +724,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       if (!ctx->dry) WCK(kcheck(ctx, launch_merge(m, st), "merge"));
     }
   }
-  return WF_OK;
+  return join_comm(ctx, st);
 }
 
 // ------------------------------------------------------------------ backward
@@ -528,9 +735,10 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   const int64_t n = g.n, E = g.E, h = g.h, team = static_cast<int64_t>(C) * n * E;
   auto off = [&](int r, int64_t per) { return ctx->emulated ? r * per : 0; };
   auto L = [&](int r, auto* p, int64_t per) { return local(ctx, r) ? p + off(r, per) : decltype(p)(nullptr); };
-  auto lp = [&](int r, auto* p) { return local(ctx, r) ? p : decltype(p)(nullptr); };
+  auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_bwd;
   tr.clear();
+  WCK(ipc_barrier(ctx, st));
 
   // D = rowsum(dO o O) on own rows (reading c12).
   for (int r = 0; r < P; ++r) {
@@ -629,7 +837,12 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         y.segs.push_back({pdq(r, s), lp(dst, B(ctx, dst).pdq[s1]), team * 4});
         dq.push_back(y);
       }
-      if (overlap) {  // the package does not depend on step s: post it first
+      if (overlap && ctx->ipc) {
+        // the package does not depend on step s: push it as soon as next released the slot
+        if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+        WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
+        WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
+      } else if (overlap) {  // the package does not depend on step s: post it first
         CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
         WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
       }
@@ -663,7 +876,15 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       prof_end(ctx, st, e0, ctx->ev_bwd);
     }
     if (s < R - 1) {
-      if (overlap) {
+      if (overlap && ctx->ipc) {
+        // dQ depends on step s: push it after the step, then release my slot
+        CK(cudaEventRecord(ctx->ev_b, st));
+        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+        WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
+        CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
+        WCK(ipc_ack(ctx, pl.last[ctx->rank], st));
+        CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
+      } else if (overlap) {
         // dQ depends on step s: after it; the receiver's next step waits for both
         CK(cudaEventRecord(ctx->ev_b, st));
         CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
@@ -680,6 +901,8 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       pkg_team = nt;
     }
   }
+
+  if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
 
   // return hop: dQ back to its home
   std::vector<float*> home(P, nullptr);
@@ -724,7 +947,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         for (int p = t * C; p < t * C + C; ++p) {
           if (p == r) continue;
           const int jp = p - t * C;
-          Xfer x{1, WF_KIND_RS_DKV, R, r, p, p, {}};
+          Xfer x{1, WF_KIND_RS_DKV, R, r, p, p, {}, ctx->ipc};
           x.segs.push_back({at(rk[r], jp * n * E), at(lp(p, B(ctx, p).rsk), j * n * E), n * E * 4});
           x.segs.push_back({at(rv[r], jp * n * E), at(lp(p, B(ctx, p).rsv), j * n * E), n * E * 4});
           ys.push_back(x);
@@ -735,8 +958,11 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     for (int r = 0; r < P; ++r) {
       const int j = r % C;
       for (int i = 0; i < C; ++i) {
-        kparts[r].push_back(i == j ? at(rk[r], i * n * E) : at(lp(r, B(ctx, r).rsk), i * n * E));
-        vparts[r].push_back(i == j ? at(rv[r], i * n * E) : at(lp(r, B(ctx, r).rsv), i * n * E));
+        const int ri = (r / C) * C + i;  // team member i holds a replica partial of my rows
+        kparts[r].push_back(i == j ? at(rk[r], i * n * E)
+                                   : ctx->ipc ? at(rk[ri], j * n * E) : at(lp(r, B(ctx, r).rsk), i * n * E));
+        vparts[r].push_back(i == j ? at(rv[r], i * n * E)
+                                   : ctx->ipc ? at(rv[ri], j * n * E) : at(lp(r, B(ctx, r).rsv), i * n * E));
       }
     }
   } else {
@@ -774,7 +1000,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       for (int p = t * C; p < t * C + C; ++p) {
         if (p == r) continue;
         const int jp = p - t * C;
-        Xfer x{1, WF_KIND_RS_DQ, R, r, p, p, {}};
+        Xfer x{1, WF_KIND_RS_DQ, R, r, p, p, {}, ctx->ipc};
         x.segs.push_back({at(home[r], jp * n * E), at(lp(p, B(ctx, p).rsq), j * n * E), n * E * 4});
         xs.push_back(x);
       }
@@ -783,8 +1009,11 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   }
   for (int r = 0; r < P; ++r) {
     const int j = r % C;
-    for (int i = 0; i < C; ++i)
-      qparts[r].push_back(i == j ? at(home[r], i * n * E) : at(lp(r, B(ctx, r).rsq), i * n * E));
+    for (int i = 0; i < C; ++i) {
+      const int ri = (r / C) * C + i;
+      qparts[r].push_back(i == j ? at(home[r], i * n * E)
+                                 : ctx->ipc ? at(home[ri], j * n * E) : at(lp(r, B(ctx, r).rsq), i * n * E));
+    }
   }
   if (ctx->dry) return WF_OK;
   for (int r = 0; r < P; ++r) {
@@ -800,7 +1029,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       WCK(kcheck(ctx, launch_sum(s, st), "sum"));
     }
   }
-  return WF_OK;
+  return join_comm(ctx, st);
 }
 
 wf_status new_ctx(int P, int C, wf_ctx** out, wf_ctx** tmp) {
@@ -820,6 +1049,7 @@ wf_status make_streams(wf_ctx* ctx) {
   CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
   return WF_OK;
 }
 
@@ -867,6 +1097,9 @@ wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, w
       wf_finalize(ctx);
       return fail(nullptr, WF_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
+    // transport: peer-memory copies + flags (default) or NCCL send/recv (WF_TRANSPORT=nccl)
+    const char* tp = std::getenv("WF_TRANSPORT");
+    ctx->ipc = !(tp && std::string(tp) == "nccl") && P <= kMaxRanks;
   }
   *out = ctx;
   return WF_OK;
@@ -990,6 +1223,21 @@ wf_status wf_shard_ranges(int P, int rank, int64_t N, int causal, int64_t ranges
 
 int64_t wf_kernel_launches(const wf_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+wf_status wf_phase_times(wf_ctx* ctx, double* ms_by_kind, int n) {
+  if (!ctx || !ms_by_kind) return fail(ctx, WF_ERR_ARG, "wf_phase_times: null");
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i) ms_by_kind[i] = 0;
+  for (auto& pr : ctx->ev_phase) {
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, pr.second.first, pr.second.second));
+    if (pr.first >= 0 && pr.first < n) ms_by_kind[pr.first] += t;
+    ctx->ev_pool.push_back(pr.second.first);
+    ctx->ev_pool.push_back(pr.second.second);
+  }
+  ctx->ev_phase.clear();
+  return WF_OK;
+}
+
 wf_status wf_set_debug(wf_ctx* ctx, int flags) {
   if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
   ctx->debug = flags;
@@ -1032,14 +1280,19 @@ wf_status wf_finalize(wf_ctx* ctx) {
   if (!ctx) return WF_OK;
   if (ctx->ws) {
     cudaDeviceSynchronize();
+    for (size_t r = 0; r < ctx->peer_base.size(); ++r)
+      if (static_cast<int>(r) != ctx->rank && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
     cudaFree(ctx->ws);
   }
+  for (cudaEvent_t e : ctx->ev_step) cudaEventDestroy(e);
+  if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   for (auto& pr : ctx->ev_fwd) ctx->ev_pool.push_back(pr.first), ctx->ev_pool.push_back(pr.second);
   for (auto& pr : ctx->ev_bwd) ctx->ev_pool.push_back(pr.first), ctx->ev_pool.push_back(pr.second);
+  for (auto& pr : ctx->ev_phase) ctx->ev_pool.push_back(pr.second.first), ctx->ev_pool.push_back(pr.second.second);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
   return WF_OK;

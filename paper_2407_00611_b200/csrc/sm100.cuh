@@ -187,6 +187,18 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = n + f, |f| <= 1/2,
+// degree-3 relative-minimax polynomial for 2^f (max rel. error 1.4e-4, far below bf16's
+// 3.9e-3), exponent added as an integer.  Used for a fraction of the softmax
+// exponentials so the MUFU unit stops being the co-bottleneck of the forward.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits hold round(x)
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -163,6 +163,12 @@ class Context:
         _check(lib().wf_kernel_times(self.h, out), self.h)
         return out[0], out[1], int(out[2]), int(out[3])
 
+    def phase_times(self):
+        """{kind: device ms} of the message phases since profiling was enabled / last call."""
+        out = (ctypes.c_double * len(KINDS))()
+        _check(lib().wf_phase_times(self.h, out, len(KINDS)), self.h)
+        return {k: out[i] for i, k in enumerate(KINDS) if out[i] > 0}
+
     def kernel_launches(self):
         return int(lib().wf_kernel_launches(self.h))
 
