@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "attn fwd+bwd TFLOP/s/GPU & tensor-pipe % vs N at 1/2/4/8 B200, C∈{1,2,4}"
-DEFAULT_C = {1: 1, 2: 2, 4: 2, 8: 2}
+DEFAULT_C = {1: 1, 2: 2, 4: 4, 8: 4}
 
 
 def parse():
@@ -35,7 +35,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wf", choices=["wf", "reference"])
-    ap.add_argument("--C", type=int, default=0, help="team size (0 = default table)")
+    ap.add_argument("--C", type=int, default=0,
+                    help="team size; 0 = the scheduler's grid search (Eq. 8, PAPER.md:302-309) at P > 1")
     ap.add_argument("--seq", type=int, default=0, help="sequence length N (0 = workload default)")
     ap.add_argument("--workload", default="gpt", choices=["gpt", "dit"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -182,7 +183,15 @@ def main():
     import paper_2407_00611_b200 as wf
 
     name, N, heads, hd, causal = workload(args, P)
-    C = args.C or DEFAULT_C.get(P, 1)
+    sched = None
+    if args.C:
+        C = args.C
+    elif P > 1:
+        from paper_2407_00611_b200 import scheduler
+        C, table = scheduler.search(P, rank, N, heads, hd, causal)
+        sched = {"search": "Eq. 8 argmax over C (PAPER.md:302-309)", "ms_per_step": table, "chosen": C}
+    else:
+        C = DEFAULT_C.get(P, 1)
     n = N // P
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     shape = (n, heads, hd)
@@ -317,6 +326,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                          "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
             "exposed_comm": exposed,
+            "scheduler": sched,
             "phase_ms_per_step": phase_ms,
             "cpu_baseline": cpu,
             "e2e": e2e,

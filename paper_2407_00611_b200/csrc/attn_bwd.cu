@@ -24,14 +24,10 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ int tile_gpos(const PosTable& t, int row0) {
-  return t.start[row0 / t.chunk] + row0 % t.chunk;
-}
-
 // for K tile at kpos0: 0 = q tile fully masked, 1 = full, 2 = diagonal
 __device__ __forceinline__ int qtile_kind(const BwdArgs& a, int kpos0, int it) {
   if (!a.causal) return 1;
-  const int qp0 = tile_gpos(a.qpos, it * WF_TILE);
+  const int qp0 = tile_gpos(a.qpos, it);
   return qp0 < kpos0 ? 0 : (qp0 == kpos0 ? 2 : 1);
 }
 
@@ -110,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kt = blockIdx.x;
   const int head = blockIdx.y;
   const int k0 = kt * WF_TILE;
-  const int kpos0 = a.causal ? tile_gpos(a.kpos, k0) : k0;
+  const int kpos0 = a.causal ? tile_gpos(a.kpos, kt) : k0;
   const int nqt = a.nq / WF_TILE;
 
   if (threadIdx.x == 0) {
@@ -427,20 +423,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           mbar_arrive(&bar[B_DQE]);
         }
-#if WF_DQ_MODE == 3
-        uint8_t* stg = stg_row + (chunk & 1) * kStgBuf;
-        if (threadIdx.x == 0) bulk_wait_read<1>();  // reduce of chunk-2 has read this buffer
-        named_bar_sync(1, 128);
+#if WF_DQ_MODE == 2  // experiment: no dQ reduction at all (timing only)
+        if (rr[0] == 0x7f800001u) a.dq_acc[0] = 1.f;
+        (void)stg_row;
+#elif WF_DQ_MODE == 3 || WF_DQ_MODE == 4
+        // per-warp staging box [32 rows][32 fp32] (4 KB, 128B-swizzled), double buffered;
+        // lane 0 issues the warp's TMA reduce: only warp-level synchronisation
+        uint8_t* wbox = smem + Cfg::OFF_STG + (chunk & 1) * kStgBuf + warp * 4096;
+        if (lane == 0) bulk_wait_read<1>();  // this warp's reduce of chunk-2 has read the box
+        __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<uint4*>(stg + ((j ^ (r & 7)) << 4)) =
+          *reinterpret_cast<uint4*>(wbox + lane * 128 + ((j ^ (lane & 7)) << 4)) =
               make_uint4(rr[4 * j], rr[4 * j + 1], rr[4 * j + 2], rr[4 * j + 3]);
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (threadIdx.x == 0) {
-          tma_reduce_add_3d(&tmDQ, smem + Cfg::OFF_STG + (chunk & 1) * kStgBuf, c0, head, it * WF_TILE);
+        __syncwarp();
+        if (lane == 0 && WF_DQ_MODE == 3) {
+          tma_reduce_add_3d(&tmDQ, wbox, c0, head, it * WF_TILE + warp * 32);
           bulk_commit();
         }
+        (void)stg_row;
 #else
         const int ncol = (D - c0) < 32 ? (D - c0) : 32;
 #pragma unroll
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++ii;
     }
-    if (threadIdx.x == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();

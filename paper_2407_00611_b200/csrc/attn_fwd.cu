@@ -28,14 +28,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
 
-__device__ __forceinline__ int tile_gpos(const PosTable& t, int row0) {
-  return t.start[row0 / t.chunk] + row0 % t.chunk;
-}
-
 // 0 = fully masked (skip), 1 = fully visible, 2 = diagonal
 __device__ __forceinline__ int tile_kind(const FwdArgs& a, int qpos0, int jt) {
   if (!a.causal) return 1;
-  int kp0 = tile_gpos(a.kpos, jt * WF_TILE);
+  int kp0 = tile_gpos(a.kpos, jt);
   return kp0 > qpos0 ? 0 : (kp0 == qpos0 ? 2 : 1);
 }
 
@@ -53,8 +49,9 @@ struct FwdCfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-// barriers: Q, K[2], V[2], KV-empty[2], S-full[2 tiles], P-full[2 tiles], O-final[2 tiles]
-enum { B_Q = 0, B_K = 1, B_V = 3, B_KVE = 5, B_S = 7, B_P = 9, B_OF = 11, B_NUM = 13 };
+// barriers: Q, K[2], V[2], KV-empty[2], S-full[2 tiles], P-full[2 tiles] (stride 4: slots for
+// a split publication of P -- measured slower, so one arrive per tile), O-final[2 tiles].
+enum { B_Q = 0, B_K = 1, B_V = 3, B_KVE = 5, B_S = 7, B_P = 9, B_OF = 17, B_NUM = 19 };
 
 constexpr int kFwdThreads = 12 * 32;  // TMA, MMA, 2 spare, 2 x 4 softmax warps
 
@@ -83,8 +80,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int q0 = pair * 2 * WF_TILE;
   const bool hasB = q0 + WF_TILE < a.nq;
   const int ntile = hasB ? 2 : 1;
-  const int qposA = a.causal ? tile_gpos(a.qpos, q0) : q0;
-  const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, q0 + WF_TILE) : q0 + WF_TILE;
+  const int qposA = a.causal ? tile_gpos(a.qpos, q0 / WF_TILE) : q0;
+  const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, q0 / WF_TILE + 1) : q0 + WF_TILE;
   const int nkt = a.nk / WF_TILE;
   const bool has_state = a.o_in != nullptr;
   // kind of (query tile t, key tile jt): 0 masked, 1 full, 2 diagonal
@@ -102,7 +99,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bar[B_V + i], 1);
       mbar_init(&bar[B_KVE + i], 1);
       mbar_init(&bar[B_S + i], 1);
-      mbar_init(&bar[B_P + i], 128);
+      for (int c = 0; c < 4; ++c) mbar_init(&bar[B_P + 4 * i + c], 128);
       mbar_init(&bar[B_OF + i], 1);
     }
     fence_barrier_init();
@@ -160,7 +157,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       };
       auto issue_pv = [&](int t, int j) {
         const int st = j & 1;
-        mbar_wait(&bar[B_P + t], j & 1);
+        mbar_wait(&bar[B_P + 4 * t], j & 1);
         if (t == 0) mbar_wait(&bar[B_V + st], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t sV = smem_u32(smem + Cfg::OFF_V + st * Cfg::TILE);
@@ -295,7 +292,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bar[B_P + t]);
+        mbar_arrive(&bar[B_P + 4 * t]);
         l += rs;
         ++j;
       }

@@ -47,7 +47,7 @@ bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int he
   if (!enc) return false;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 4, static_cast<cuuint64_t>(heads) * D * 4};
-  cuuint32_t box[3] = {32, 1, WF_TILE};
+  cuuint32_t box[3] = {32, 1, 32};  // one warp's 32 query rows x 32 fp32 columns
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -61,11 +61,13 @@ bool fill_postable(PosTable* t, int rows, int chunk, const int32_t* starts, int 
     t->chunk = rows;
     t->nchunks = 1;
     t->start[0] = 0;
+    t->tpc_shift = tpc_shift_of(rows);
     return true;
   }
   if (chunk % WF_TILE || n <= 0 || n > WF_MAX_CHUNKS || static_cast<int64_t>(n) * chunk != rows) return false;
   t->chunk = chunk;
   t->nchunks = n;
+  t->tpc_shift = tpc_shift_of(chunk);
   for (int i = 0; i < n; ++i) t->start[i] = starts[i];
   return true;
 }

@@ -24,8 +24,26 @@ __host__ __device__ __forceinline__ int64_t stat_index(int head, int row, int he
 struct PosTable {
   int chunk;                      // rows per chunk (multiple of 128)
   int nchunks;
+  int tpc_shift;                  // log2(chunk / 128) when that is a power of two, else -1
   int start[WF_MAX_CHUNKS];       // global start of each chunk
 };
+
+// Global position of the first row of 128-row tile `tile` (no integer division on the
+// power-of-two fast path: it runs once per tile in every warp role).
+__host__ __device__ __forceinline__ int tile_gpos(const PosTable& t, int tile) {
+  if (t.tpc_shift >= 0) {
+    const int c = tile >> t.tpc_shift;
+    return t.start[c] + ((tile - (c << t.tpc_shift)) << 7);
+  }
+  const int row0 = tile * 128;
+  return t.start[row0 / t.chunk] + row0 % t.chunk;
+}
+inline int tpc_shift_of(int chunk) {
+  const int tpc = chunk / 128;
+  int sh = 0;
+  while ((1 << sh) < tpc) ++sh;
+  return (1 << sh) == tpc ? sh : -1;
+}
 
 // Arguments of one block-forward launch (PAPER.md:183 forward_iteration):
 // the (O, lse) state of the query rows is merged with attention against one K/V block.
@@ -63,7 +81,7 @@ struct BwdArgs {
 
 // Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.
 bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
-// Host: 3-D TMA map over a [rows, heads, D] fp32 tensor, box {32, 1, 128}, SW128 (dQ reduce-add).
+// Host: 3-D TMA map over a [rows, heads, D] fp32 tensor, box {32, 1, 32}, SW128 (dQ reduce-add).
 bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,

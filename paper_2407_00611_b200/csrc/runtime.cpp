@@ -188,6 +188,7 @@ PosTable units_table(const Geo& g, int u0, int count) {
     }
   }
   t.nchunks = k;
+  t.tpc_shift = tpc_shift_of(t.chunk);
   return t;
 }
 
