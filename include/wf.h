@@ -138,6 +138,12 @@ wf_status wf_phase_times(wf_ctx* ctx, double* ms_by_kind, int n);
 #define WF_DEBUG_NO_TRANSFER 1
 wf_status wf_set_debug(wf_ctx* ctx, int flags);
 
+/* Debug aid: record clock64() stamps of the block kernels' warp roles for CTA (cta, head 0)
+ * of every launch (cta < 0: off); read n words after the launches (layout: slot
+ * (role * 1024 + tile) * 8 + event, see csrc/attn_fwd.cu / attn_bwd.cu). */
+wf_status wf_debug_timeline(int cta);
+wf_status wf_debug_timeline_read(unsigned long long* out, size_t n);
+
 /* Last error text of ctx (or of the last context-less call when ctx is NULL). */
 const char* wf_last_error(const wf_ctx* ctx);
 

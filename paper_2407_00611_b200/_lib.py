@@ -44,6 +44,8 @@ _SIGS = {
     "wf_set_debug": (c_int, [c_p, c_int]),
     "wf_phase_times": (c_int, [c_p, ctypes.POINTER(ctypes.c_double), c_int]),
     "wf_kernel_times": (c_int, [c_p, ctypes.POINTER(ctypes.c_double)]),
+    "wf_debug_timeline": (c_int, [c_int]),
+    "wf_debug_timeline_read": (c_int, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t]),
     "wf_last_error": (ctypes.c_char_p, [c_p]),
     "wf_finalize": (c_int, [c_p]),
     "wf_block_fwd": (c_int, [c_p, c_p, c_p, c_int, c_int, c_int, c_int, c_int, c_int, c_i32p, c_int, c_i32p, c_int,

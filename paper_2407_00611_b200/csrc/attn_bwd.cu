@@ -31,30 +31,28 @@ __device__ __forceinline__ int qtile_kind(const BwdArgs& a, int kpos0, int it) {
   return qp0 < kpos0 ? 0 : (qp0 == kpos0 ? 2 : 1);
 }
 
-constexpr int kStgBuf = 128 * 128;       // one dQ staging buffer: [128 rows][32 fp32], 128B-swizzled
-constexpr int kStgBufs = 2;
-
 template <int D>
 struct BwdCfg {
   static constexpr int DP = (D + 15) / 16 * 16;
   static constexpr int NP = (D + 63) / 64;
   static constexpr int PANEL = 128 * 128;
   static constexpr int TILE = NP * PANEL;
+  static constexpr int QST = 2;                 // query-tile ring depth
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = TILE;
-  static constexpr int OFF_Q = 2 * TILE;        // 2 stages
-  static constexpr int OFF_DO = 4 * TILE;       // 1 stage
-  static constexpr int OFF_DS = 5 * TILE;       // [128 q] x [128 kv] bf16, MN-major SW128 (2 panels)
-  static constexpr int OFF_STG = OFF_DS + 2 * PANEL;   // dQ staging: kStgBufs x [128 rows][32 fp32]
-  static constexpr int OFF_STAT = OFF_STG + kStgBufs * kStgBuf;  // 2 stages x (lse[128], dsum[128]) fp32
+  static constexpr int OFF_Q = 2 * TILE;        // QST stages
+  static constexpr int OFF_DO = (2 + QST) * TILE;  // 1 stage
+  static constexpr int OFF_DS = (3 + QST) * TILE;     // [128 kv] x [128 q] bf16 dS (2 SW128 panels)
+  static constexpr int OFF_STG = OFF_DS + 2 * PANEL;  // dQ drain staging: per warp 2 x [32 rows][32 fp32]
+  static constexpr int OFF_STAT = OFF_STG + 32768;    // 2 stages x (lse[128], dsum[128]) fp32
   static constexpr int OFF_BAR = OFF_STAT + 2 * 1024;
-  static constexpr int SMEM = OFF_BAR + 256;
+  static constexpr int SMEM = OFF_BAR + 192;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 enum {
-  B_KV = 0, B_QF = 1, B_QE = 3, B_DOF = 5, B_DOE = 6, B_S = 7, B_DP = 8, B_P = 9, B_DS = 10, B_DQF = 11,
-  B_DQE = 12, B_DSE = 13, B_DONE = 14, B_NUM = 15
+  B_KV = 0, B_QF = 1, B_QE = 4, B_SF = 7, B_SE = 9, B_DOF = 11, B_DOE = 12, B_S = 13, B_DP = 14, B_P = 15,
+  B_DS = 16, B_DQF = 17, B_DQE = 18, B_DSE = 19, B_DONE = 20, B_NUM = 21
 };
 
 constexpr int kThreads = 14 * 32;  // 4 dQ-drain + 8 compute + TMA + MMA warps
@@ -63,13 +61,7 @@ constexpr int kCompute = 256;
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// global[dst, dst + bytes) += shared[src, src + bytes) (fp32), completed per bulk group
-__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_u32(ssrc)), "r"(bytes)
-               : "memory");
-}
-// TMA tensor reduce-add of a [128 rows][32 fp32] SW128 smem box into global (fp32)
+// TMA tensor reduce-add of a [32 rows][32 fp32] SW128 smem box into global (fp32)
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* ssrc, int c0, int c1, int c2) {
   asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -96,6 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ BwdArgs a) {
   using Cfg = BwdCfg<D>;
   constexpr int DP = Cfg::DP;
+  constexpr int QST = Cfg::QST;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BAR + B_NUM * 8);
@@ -108,13 +101,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int k0 = kt * WF_TILE;
   const int kpos0 = a.causal ? tile_gpos(a.kpos, kt) : k0;
   const int nqt = a.nq / WF_TILE;
+  const bool tlon = a.tl && blockIdx.x == a.tl_cta && blockIdx.y == 0;
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
     mbar_init(&bar[B_KV], 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QST; ++i) {
       mbar_init(&bar[B_QF + i], 1);
       mbar_init(&bar[B_QE + i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar[B_SF + i], 1);
+      mbar_init(&bar[B_SE + i], kCompute);
     }
     mbar_init(&bar[B_DOF], 1);
     mbar_init(&bar[B_DOE], 1);
@@ -138,12 +136,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 12) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producers
+    // lane 0: K, V once, then the query ring (QST stages, freed by dK);
+    // lane 1: the statistics ring (2 stages, freed by the compute warps) and dO (freed by dV).
     if (lane == 0) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      tma_prefetch_desc(&tmDO);
       mbar_arrive_expect_tx(&bar[B_KV], 2 * Cfg::TILE);
       for (int p = 0; p < Cfg::NP; ++p) {
         tma_load_3d(smem + Cfg::OFF_K + p * Cfg::PANEL, &tmK, &bar[B_KV], p * 64, head, k0);
@@ -152,16 +151,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ii = 0;
       for (int it = 0; it < nqt; ++it) {
         if (qtile_kind(a, kpos0, it) == 0) continue;
-        const int st = ii & 1;
-        if (ii >= 2) mbar_wait(&bar[B_QE + st], ((ii - 2) >> 1) & 1);
-        mbar_arrive_expect_tx(&bar[B_QF + st], Cfg::TILE + 1024);
+        const int st = ii % QST;
+        if (ii >= QST) mbar_wait(&bar[B_QE + st], ((ii - QST) / QST) & 1);
+        tl_stamp(a.tl, tlon, 3, ii, 0);
+        mbar_arrive_expect_tx(&bar[B_QF + st], Cfg::TILE);
         for (int p = 0; p < Cfg::NP; ++p)
           tma_load_3d(smem + Cfg::OFF_Q + st * Cfg::TILE + p * Cfg::PANEL, &tmQ, &bar[B_QF + st], p * 64, head,
                       it * WF_TILE);
+        ++ii;
+      }
+    } else if (lane == 1) {
+      tma_prefetch_desc(&tmDO);
+      int ii = 0;
+      for (int it = 0; it < nqt; ++it) {
+        if (qtile_kind(a, kpos0, it) == 0) continue;
+        const int ss = ii & 1;
+        if (ii >= 2) mbar_wait(&bar[B_SE + ss], ((ii - 2) >> 1) & 1);
+        mbar_arrive_expect_tx(&bar[B_SF + ss], 1024);
         const int64_t soff = stat_index(head, it * WF_TILE, a.heads, a.stat_blk);
-        bulk_load(stat + st * 256, a.lse + soff, 512, &bar[B_QF + st]);
-        bulk_load(stat + st * 256 + 128, a.dsum + soff, 512, &bar[B_QF + st]);
+        bulk_load(stat + ss * 256, a.lse + soff, 512, &bar[B_SF + ss]);
+        bulk_load(stat + ss * 256 + 128, a.dsum + soff, 512, &bar[B_SF + ss]);
         if (ii >= 1) mbar_wait(&bar[B_DOE], (ii - 1) & 1);
+        tl_stamp(a.tl, tlon, 3, ii, 1);
         mbar_arrive_expect_tx(&bar[B_DOF], Cfg::TILE);
         for (int p = 0; p < Cfg::NP; ++p)
           tma_load_3d(smem + Cfg::OFF_DO + p * Cfg::PANEL, &tmDO, &bar[B_DOF], p * 64, head, it * WF_TILE);
@@ -170,21 +181,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
-    // Order per query tile i: dP_i, [P_i] dV_i, S_{i+1}, [dS_i] dK_i, dQ_i.  S_{i+1} is
-    // issued as soon as dV_i has consumed P_i from TMEM, so the compute warps' exp work
-    // of tile i+1 overlaps the dK_i / dQ_i MMAs.
+    // Per query tile i: dP_i, [P_i] dV_i, S_{i+1}, [dS_i] dQ_i, dK_i.  S_{i+1} is issued as
+    // soon as dV_i has consumed P_i from TMEM, so the compute warps' exp work of tile i+1
+    // overlaps dQ_i / dK_i; dQ first so that its drain (which gates dP_{i+1}) starts early.
     if (lane == 0) {
       constexpr uint32_t idSP = idesc_bf16_f32(128, 128, 0, 0);   // K x Q^T, V x dO^T (both K-major)
-      constexpr uint32_t idKV = idesc_bf16_f32(128, DP, 0, 1);    // P^T/dS^T (TMEM) x dO/Q (MN-major)
+      constexpr uint32_t idKV = idesc_bf16_f32(128, DP, 0, 1);    // P^T (TMEM) / dS^T (smem) x dO / Q (MN-major)
       constexpr uint32_t idQ = idesc_bf16_f32(128, DP, 1, 1);     // dS (smem, MN-major) x K (MN-major)
       const uint32_t sK = smem_u32(smem + Cfg::OFF_K);
       const uint32_t sV = smem_u32(smem + Cfg::OFF_V);
       const uint32_t sDO = smem_u32(smem + Cfg::OFF_DO);
       const uint32_t sDS = smem_u32(smem + Cfg::OFF_DS);
       auto issue_s = [&](int i) {
-        const int st = i & 1;
+        const int st = i % QST;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
-        mbar_wait(&bar[B_QF + st], (i >> 1) & 1);
+        mbar_wait(&bar[B_QF + st], (i / QST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
@@ -200,12 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (ntiles > 0) issue_s(0);
       for (int ii = 0; ii < ntiles; ++ii) {
-        const int st = ii & 1;
+        const int st = ii % QST;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
         // dP^T = V dO^T (the dP region must be drained of the previous dQ)
         mbar_wait(&bar[B_DOF], ii & 1);
         if (ii >= 1) mbar_wait(&bar[B_DQE], (ii - 1) & 1);
         tc_fence_after();
+        tl_stamp(a.tl, tlon, 0, ii, 0);
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
           const int p = k >> 2, kk = k & 3;
@@ -216,31 +228,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         // dV += P^T dO
         mbar_wait(&bar[B_P], ii & 1);
         tc_fence_after();
+        tl_stamp(a.tl, tlon, 0, ii, 1);
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
           mma_ts(tbase + 128, tbase + 0 + k * 8, smem_desc_sw128(sDO + k * 2048, Cfg::PANEL, 1024), idKV,
                  (ii > 0 || k > 0) ? 1u : 0u);
         mma_commit(&bar[B_DOE]);
         if (ii + 1 < ntiles) issue_s(ii + 1);
-        // dK += dS^T Q ; dQ = dS K
+        tl_stamp(a.tl, tlon, 0, ii, 2);
+        // dQ = dS K (dS as the MN-major A), then dK += dS^T Q (dS as the K-major A)
         mbar_wait(&bar[B_DS], ii & 1);
         tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < WF_TILE / 16; ++k)
-          mma_ts(tbase + 384, tbase + 256 + k * 8, smem_desc_sw128(sQ + k * 2048, Cfg::PANEL, 1024), idKV,
-                 (ii > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&bar[B_QE + st]);
+        tl_stamp(a.tl, tlon, 0, ii, 3);
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
           mma_ss(tbase + 256, smem_desc_sw128(sDS + k * 2048, Cfg::PANEL, 1024),
                  smem_desc_sw128(sK + k * 2048, Cfg::PANEL, 1024), idQ, k > 0 ? 1u : 0u);
         mma_commit(&bar[B_DQF]);
+#pragma unroll
+        for (int k = 0; k < WF_TILE / 16; ++k)
+          mma_ss(tbase + 384, smem_desc_sw128(sDS + (k >> 2) * Cfg::PANEL + (k & 3) * 32, 16, 1024),
+                 smem_desc_sw128(sQ + k * 2048, Cfg::PANEL, 1024), idKV, (ii > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&bar[B_QE + st]);
         mma_commit(&bar[B_DSE]);
       }
       mma_commit(&bar[B_DONE]);
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ compute: P^T, dS^T
+    // ------------------------------------------------------------ compute: P^T, dS
     // 8 warps: warp w covers TMEM lane quadrant w % 4 (key rows) and query columns
     // [64 h, 64 h + 64), h = (w - 4) / 4.
     const int wq = warp & 3;
@@ -252,14 +267,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; it < nqt; ++it) {
       const int kind = qtile_kind(a, kpos0, it);
       if (kind == 0) continue;
-      const int st = ii & 1;
-      const float* slse = stat + st * 256 + hf * 64;
-      const float* sdd = stat + st * 256 + 128 + hf * 64;
-      mbar_wait(&bar[B_QF + st], (ii >> 1) & 1);  // stats landed
+      const int ss = ii & 1;
+      const float* slse = stat + ss * 256 + hf * 64;
+      const float* sdd = stat + ss * 256 + 128 + hf * 64;
+      mbar_wait(&bar[B_SF + ss], (ii >> 1) & 1);  // stats landed
       {
         // convert the tile's statistics once: lse -> lse * log2(e) (+inf for query rows
         // with no key at all, so exp2 gives 0 without a branch), D -> D / sqrt(d)
-        float* sst = stat + st * 256;
+        float* sst = stat + ss * 256;
         const int tc = threadIdx.x - 128;
         const float x = sst[tc];
         sst[tc] = tc < 128 ? (x == -INFINITY ? INFINITY : x * kLog2e) : x * a.scale;
@@ -267,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&bar[B_S], ii & 1);
       tc_fence_after();
+      tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 0);
       uint32_t pk[32];  // P^T row, this half: 64 bf16
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -296,10 +312,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar[B_P]);
-      // dS^T = P^T o (dP^T - D), pre-scaled by 1/sqrt(d) for both dK and dQ
+      tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 1);
+      // dS = P o (dP - D), pre-scaled by 1/sqrt(d) for both dK and dQ
       mbar_wait(&bar[B_DP], ii & 1);
       tc_fence_after();
-      if (ii >= 1) mbar_wait(&bar[B_DSE], (ii - 1) & 1);
+      if (ii >= 1) mbar_wait(&bar[B_DSE], (ii - 1) & 1);  // dQ/dK of tile ii-1 have read dS
+      tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 2);
       uint32_t dk[32];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -315,16 +333,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           dk[c * 16 + i] = pack_bf16x2(d0, d1);
         }
       }
-      tmem_st32(tl + 256 + hf * 32, dk);
-      // dS -> smem (A of dQ = dS K, MN-major SW128): this half's 64 q = panel hf, row r
+      // dS -> smem (A of both dK and dQ): this half's 64 q = panel hf, row r
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         *reinterpret_cast<uint4*>(sds + ((j ^ (r & 7)) << 4)) =
             make_uint4(dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       fence_proxy_async_smem();
-      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar[B_DS]);
+      mbar_arrive(&bar[B_SE + ss]);
+      tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 3);
       ++ii;
     }
     // epilogue: dK, dV of this key tile (this warp's half of the 16-column chunks)
@@ -386,74 +404,76 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ dQ drain (warps 0-3)
-    // TMEM -> registers -> this thread's 128-byte staging row -> bulk reduce-add into the
-    // fp32 dQ accumulator in global memory (one full-line L2 reduction per row chunk).
+    // TMEM -> registers (two 64-column halves; the region is released right after the
+    // second half is read) -> this warp's double-buffered staging boxes [32 rows][32 fp32]
+    // (128B swizzle, 16-byte chunk j at j ^ (row & 7): conflict-free) -> one TMA tensor
+    // reduce-add per box into the fp32 dQ accumulator.
     const int r = warp * 32 + lane;  // query row within the tile
     const uint32_t tl = tbase + (static_cast<uint32_t>(warp * 32) << 16);
-#ifndef WF_DQ_MODE
-#define WF_DQ_MODE 3
-#endif
-    // Each thread writes its query row's 32 columns into a 128B-swizzled staging row
-    // (16-byte chunk j at j ^ (r & 7): conflict-free), then one thread reduce-adds the
-    // [128 x 32] box into the fp32 dQ accumulator with a TMA tensor reduction.
-    uint8_t* stg_row = smem + Cfg::OFF_STG + r * 128;
+    uint8_t* wbox0 = smem + Cfg::OFF_STG + warp * 8192;
     int ii = 0, chunk = 0;
     for (int it = 0; it < nqt; ++it) {
       if (qtile_kind(a, kpos0, it) == 0) continue;
       mbar_wait(&bar[B_DQF], ii & 1);
       tc_fence_after();
-#if WF_DQ_MODE == 0
-      float* dst = a.dq_acc + (static_cast<size_t>(it * WF_TILE + r) * a.heads + head) * D;
-#endif
+      tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 0);
 #pragma unroll
-      for (int c0 = 0; c0 < DP; c0 += 32, ++chunk) {
-        uint32_t rr[32];
-        if (c0 + 32 <= DP) {
-          tmem_ld32(tl + 256 + c0, rr);
-        } else {
-          uint32_t r16[16];
-          tmem_ld16(tl + 256 + c0, r16);
+      for (int half = 0; half < 2; ++half) {
+        const int cbase = half * 64;
+        if (cbase < DP) {
+          uint32_t ra[32], rb[32];
+          const bool two = cbase + 32 < DP;
+          if (cbase + 32 <= DP) {
+            tmem_ld32(tl + 256 + cbase, ra);
+          } else {
+            uint32_t r16[16];
+            tmem_ld16(tl + 256 + cbase, r16);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) rr[i] = r16[i];
+            for (int i = 0; i < 16; ++i) ra[i] = r16[i];
 #pragma unroll
-          for (int i = 16; i < 32; ++i) rr[i] = 0u;
+            for (int i = 16; i < 32; ++i) ra[i] = 0u;
+          }
+          if (two) {
+            if (cbase + 64 <= DP) {
+              tmem_ld32(tl + 256 + cbase + 32, rb);
+            } else {
+              uint32_t r16[16];
+              tmem_ld16(tl + 256 + cbase + 32, r16);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) rb[i] = r16[i];
+#pragma unroll
+              for (int i = 16; i < 32; ++i) rb[i] = 0u;
+            }
+          }
+          tmem_wait_ld();
+          if (cbase + 64 >= DP) {  // last TMEM read of this tile: release the dQ region
+            tc_fence_before();
+            mbar_arrive(&bar[B_DQE]);
+            tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 1);
+          }
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            if (sub == 1 && !two) break;
+            const int c0 = cbase + 32 * sub;
+            const uint32_t* rr = sub == 0 ? ra : rb;
+            uint8_t* wbox = wbox0 + (chunk & 1) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the reduce of chunk-2 has read this box
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(wbox + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(rr[4 * j], rr[4 * j + 1], rr[4 * j + 2], rr[4 * j + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_3d(&tmDQ, wbox, c0, head, it * WF_TILE + warp * 32);
+              bulk_commit();
+            }
+            ++chunk;
+          }
         }
-        tmem_wait_ld();
-        if (c0 + 32 >= DP) {  // last TMEM read of this tile: release the dQ region
-          tc_fence_before();
-          mbar_arrive(&bar[B_DQE]);
-        }
-#if WF_DQ_MODE == 2  // experiment: no dQ reduction at all (timing only)
-        if (rr[0] == 0x7f800001u) a.dq_acc[0] = 1.f;
-        (void)stg_row;
-#elif WF_DQ_MODE == 3 || WF_DQ_MODE == 4
-        // per-warp staging box [32 rows][32 fp32] (4 KB, 128B-swizzled), double buffered;
-        // lane 0 issues the warp's TMA reduce: only warp-level synchronisation
-        uint8_t* wbox = smem + Cfg::OFF_STG + (chunk & 1) * kStgBuf + warp * 4096;
-        if (lane == 0) bulk_wait_read<1>();  // this warp's reduce of chunk-2 has read the box
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<uint4*>(wbox + lane * 128 + ((j ^ (lane & 7)) << 4)) =
-              make_uint4(rr[4 * j], rr[4 * j + 1], rr[4 * j + 2], rr[4 * j + 3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && WF_DQ_MODE == 3) {
-          tma_reduce_add_3d(&tmDQ, wbox, c0, head, it * WF_TILE + warp * 32);
-          bulk_commit();
-        }
-        (void)stg_row;
-#else
-        const int ncol = (D - c0) < 32 ? (D - c0) : 32;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j * 4 < ncol)
-            atomicAdd(reinterpret_cast<float4*>(dst + c0) + j,
-                      make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
-                                  __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3])));
-        (void)stg_row;
-#endif
       }
+      tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 2);
       ++ii;
     }
     if (lane == 0) bulk_wait<0>();
@@ -474,7 +494,10 @@ cudaError_t launch_bwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr_set = true;
   }
   dim3 grid(a.nk / WF_TILE, a.heads);
-  wf_block_bwd_kernel<D><<<grid, kThreads, Cfg::SMEM, s>>>(tq, tk, tv, tdo, tdq, a);
+  BwdArgs b = a;
+  b.tl = timeline_buffer();
+  b.tl_cta = timeline_cta();
+  wf_block_bwd_kernel<D><<<grid, kThreads, Cfg::SMEM, s>>>(tq, tk, tv, tdo, tdq, b);
   return cudaGetLastError();
 }
 

@@ -42,16 +42,17 @@ struct FwdCfg {
   static constexpr int PANEL = 128 * 128;         // bytes of one [128 rows x 64 bf16] panel
   static constexpr int TILE = NP * PANEL;
   static constexpr int OFF_Q = 0;                 // 2 query tiles
-  static constexpr int OFF_K = 2 * TILE;          // 2 stages
-  static constexpr int OFF_V = 4 * TILE;          // 2 stages
-  static constexpr int OFF_BAR = 6 * TILE;
+  static constexpr int OFF_K = 2 * TILE;          // 3 stages (released after the S MMAs)
+  static constexpr int OFF_V = 5 * TILE;          // 2 stages (released after the P V MMAs)
+  static constexpr int OFF_BAR = 7 * TILE;
   static constexpr int SMEM = OFF_BAR + 256;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 // barriers: Q, K[2], V[2], KV-empty[2], S-full[2 tiles], P-full[2 tiles] (stride 4: slots for
 // a split publication of P -- measured slower, so one arrive per tile), O-final[2 tiles].
-enum { B_Q = 0, B_K = 1, B_V = 3, B_KVE = 5, B_S = 7, B_P = 9, B_OF = 17, B_NUM = 19 };
+enum { B_Q = 0, B_K = 1, B_KE = 4, B_V = 7, B_VE = 9, B_S = 11, B_P = 13, B_OF = 21, B_NUM = 23 };
+constexpr int kKStages = 3;
 
 constexpr int kFwdThreads = 12 * 32;  // TMA, MMA, 2 spare, 2 x 4 softmax warps
 
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, q0 / WF_TILE + 1) : q0 + WF_TILE;
   const int nkt = a.nk / WF_TILE;
   const bool has_state = a.o_in != nullptr;
+  const bool tlon = a.tl && blockIdx.x == a.tl_cta && blockIdx.y == 0;
   // kind of (query tile t, key tile jt): 0 masked, 1 full, 2 diagonal
   auto kind_of = [&](int t, int jt) -> int {
     if (t == 1 && !hasB) return 0;
@@ -94,10 +96,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
     mbar_init(&bar[B_Q], 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       mbar_init(&bar[B_K + i], 1);
+      mbar_init(&bar[B_KE + i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&bar[B_V + i], 1);
-      mbar_init(&bar[B_KVE + i], 1);
+      mbar_init(&bar[B_VE + i], 1);
       mbar_init(&bar[B_S + i], 1);
       for (int c = 0; c < 4; ++c) mbar_init(&bar[B_P + 4 * i + c], 128);
       mbar_init(&bar[B_OF + i], 1);
@@ -114,11 +119,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producers
+    // lane 0: Q and the K ring (3 stages, freed by the S MMAs); lane 1: the V ring
+    // (2 stages, freed by the P V MMAs).  Separate lanes keep a K load from queueing
+    // behind a V stage that is still being read.
     if (lane == 0) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
       mbar_arrive_expect_tx(&bar[B_Q], ntile * Cfg::TILE);
       for (int t = 0; t < ntile; ++t)
         for (int p = 0; p < Cfg::NP; ++p)
@@ -127,12 +134,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int jj = 0;
       for (int jt = 0; jt < nkt; ++jt) {
         if (!visible(jt)) continue;
-        const int st = jj & 1;
-        if (jj >= 2) mbar_wait(&bar[B_KVE + st], ((jj - 2) >> 1) & 1);
+        const int st = jj % kKStages;
+        if (jj >= kKStages) mbar_wait(&bar[B_KE + st], ((jj - kKStages) / kKStages) & 1);
+        tl_stamp(a.tl, tlon, 3, jj, 0);
         uint8_t* sk = smem + Cfg::OFF_K + st * Cfg::TILE;
-        uint8_t* sv = smem + Cfg::OFF_V + st * Cfg::TILE;
         mbar_arrive_expect_tx(&bar[B_K + st], Cfg::TILE);
         for (int p = 0; p < Cfg::NP; ++p) tma_load_3d(sk + p * Cfg::PANEL, &tmK, &bar[B_K + st], p * 64, head, jt * WF_TILE);
+        ++jj;
+      }
+    } else if (lane == 1) {
+      tma_prefetch_desc(&tmV);
+      int jj = 0;
+      for (int jt = 0; jt < nkt; ++jt) {
+        if (!visible(jt)) continue;
+        const int st = jj & 1;
+        if (jj >= 2) mbar_wait(&bar[B_VE + st], ((jj - 2) >> 1) & 1);
+        uint8_t* sv = smem + Cfg::OFF_V + st * Cfg::TILE;
         mbar_arrive_expect_tx(&bar[B_V + st], Cfg::TILE);
         for (int p = 0; p < Cfg::NP; ++p) tma_load_3d(sv + p * Cfg::PANEL, &tmV, &bar[B_V + st], p * 64, head, jt * WF_TILE);
         ++jj;
@@ -144,7 +161,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);  // Q (K-major) x K (K-major)
       constexpr uint32_t idO = idesc_bf16_f32(128, DP, 0, 1);   // P (TMEM) x V (MN-major)
       auto issue_s = [&](int t, int j) {
-        const int st = j & 1;
+        const int st = j % kKStages;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + t * Cfg::TILE);
         const uint32_t sK = smem_u32(smem + Cfg::OFF_K + st * Cfg::TILE);
 #pragma unroll
@@ -170,21 +187,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int jt = 0; jt < nkt; ++jt) nvis += visible(jt);
       mbar_wait(&bar[B_Q], 0);
       for (int j = 0; j < nvis; ++j) {
-        const int st = j & 1;
-        mbar_wait(&bar[B_K + st], (j >> 1) & 1);
-        tc_fence_after();
+        tl_stamp(a.tl, tlon, 0, j, 0);
         for (int t = 0; t < ntile; ++t) {
           if (j > 0) issue_pv(t, j - 1);
+          tl_stamp(a.tl, tlon, 0, j, 1 + 2 * t);
+          if (t == 0) {
+            mbar_wait(&bar[B_K + j % kKStages], (j / kKStages) & 1);
+            tc_fence_after();
+          }
           issue_s(t, j);
+          tl_stamp(a.tl, tlon, 0, j, 2 + 2 * t);
         }
-        if (j > 0) mma_commit(&bar[B_KVE + ((j - 1) & 1)]);
+        if (j > 0) mma_commit(&bar[B_VE + ((j - 1) & 1)]);
+        mma_commit(&bar[B_KE + j % kKStages]);
       }
       if (nvis > 0) {
         for (int t = 0; t < ntile; ++t) {
           issue_pv(t, nvis - 1);
           mma_commit(&bar[B_OF + t]);
         }
-        mma_commit(&bar[B_KVE + ((nvis - 1) & 1)]);
+        mma_commit(&bar[B_VE + ((nvis - 1) & 1)]);
       } else {
         for (int t = 0; t < ntile; ++t) mma_commit(&bar[B_OF + t]);
       }
@@ -224,6 +246,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int kind = kind_of(t, jt);
         mbar_wait(&bar[B_S + t], j & 1);
         tc_fence_after();
+        tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 0);
         float s[128];
         {
           uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -293,6 +316,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar[B_P + 4 * t]);
+        tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 1);
         l += rs;
         ++j;
       }
@@ -354,7 +378,10 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr_set = true;
   }
   dim3 grid((a.nq / WF_TILE + 1) / 2, a.heads);
-  wf_block_fwd_kernel<D><<<grid, kFwdThreads, Cfg::SMEM, s>>>(tq, tk, tv, a);
+  FwdArgs b = a;
+  b.tl = timeline_buffer();
+  b.tl_cta = timeline_cta();
+  wf_block_fwd_kernel<D><<<grid, kFwdThreads, Cfg::SMEM, s>>>(tq, tk, tv, b);
   return cudaGetLastError();
 }
 

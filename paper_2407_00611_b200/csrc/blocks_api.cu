@@ -55,6 +55,11 @@ bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int he
   return r == CUDA_SUCCESS;
 }
 
+static unsigned long long* g_tl = nullptr;
+static int g_tl_cta = 0;
+unsigned long long* timeline_buffer() { return g_tl; }
+int timeline_cta() { return g_tl_cta; }
+
 bool fill_postable(PosTable* t, int rows, int chunk, const int32_t* starts, int n) {
   std::memset(t, 0, sizeof(*t));
   if (chunk <= 0) {  // contiguous [0, rows)
@@ -81,6 +86,30 @@ const char* wf_static_error() { return g_err; }
 static wf_status set_err(wf_status s, const char* msg) {
   std::snprintf(g_err, sizeof(g_err), "%s", msg);
   return s;
+}
+
+// Debug aid: enable (cta >= 0) / disable (cta < 0) the block-kernel timeline of CTA
+// (cta, head 0); wf_debug_timeline_read copies n words (after a device synchronize).
+extern "C" wf_status wf_debug_timeline(int cta) {
+  if (cta < 0) {
+    g_tl = nullptr;
+    return WF_OK;
+  }
+  static unsigned long long* buf = nullptr;
+  const size_t bytes = size_t(4) * WF_TL_TILES * 8 * sizeof(unsigned long long);
+  if (!buf && cudaMalloc(&buf, bytes) != cudaSuccess) return set_err(WF_ERR_CUDA, "timeline alloc");
+  cudaMemset(buf, 0, bytes);
+  g_tl = buf;
+  g_tl_cta = cta;
+  return WF_OK;
+}
+extern "C" wf_status wf_debug_timeline_read(unsigned long long* out, size_t n) {
+  if (!g_tl) return set_err(WF_ERR_ARG, "timeline off");
+  if (cudaDeviceSynchronize() != cudaSuccess) return set_err(WF_ERR_CUDA, "sync");
+  const size_t cap = size_t(4) * WF_TL_TILES * 8;
+  if (cudaMemcpy(out, g_tl, (n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_err(WF_ERR_CUDA, "timeline copy");
+  return WF_OK;
 }
 
 extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, int nq, int nk, int heads,

@@ -58,6 +58,8 @@ struct FwdArgs {
   __nv_bfloat16* o_out_bf16;      // final out (bf16) or null
   float* lse_out;                 // [heads, nq]
   int lse_blk;                    // lse layout: rows in blocks of lse_blk, [nq/blk][heads][blk]
+  unsigned long long* tl;         // debug timeline (null = off), see wf_debug_timeline
+  int tl_cta;
 };
 
 // Arguments of one block-backward launch (flash-attention backward):
@@ -77,10 +79,17 @@ struct BwdArgs {
   __nv_bfloat16* dv_out;
   int dkv_accumulate;             // 1: dk_acc += ; 0: dk_acc =
   int stat_blk;                   // lse/dsum layout: [nq/blk][heads][blk]
+  unsigned long long* tl;         // debug timeline (null = off)
+  int tl_cta;
 };
 
 // Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.
 bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
+// Debug timeline (bench/profiling aid): when enabled, one CTA of every block kernel records
+// clock64() stamps at slot ((role * WF_TL_TILES + tile) * 8 + event).
+#define WF_TL_TILES 1024
+unsigned long long* timeline_buffer();  // null when disabled
+int timeline_cta();
 // Host: 3-D TMA map over a [rows, heads, D] fp32 tensor, box {32, 1, 32}, SW128 (dQ reduce-add).
 bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
 
