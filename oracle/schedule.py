@@ -14,8 +14,9 @@ Backward = §3.2.1 "Backward Propagation": K/V outer loop
 stationary on the init-shuffle block, Q inner loop: the Q-package (Q, dO, LSE, D)
 and its dQ circulate along the sub-ring (RING_QPKG, RING_DQ), then one extra P2P
 returns dQ home (RET_DQ; reading c10).  The paper is silent on where dK/dV go
-(reading c11): reverse shuffle to init_recv (REV_DKV) then team reduce-scatter
-sums (RS_DKV, RS_DQ).
+(reading c11, revised): each holder of a stationary block sends every unit's rows of
+its dK/dV partial straight to the unit's owner, who sums the C replicas (REV_DKV);
+dQ is summed by a team reduce-scatter (RS_DQ).
 Extension regime C^2 > P (reading c2, ours): R = 1, only Q (and dO, stats) are
 team-gathered; member a pulls K/V slice a = units [a P/C, (a+1) P/C) from their
 owners (SLICE_KV); dK/dV partials go straight back to the owners (REV_DKV).
@@ -299,14 +300,21 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
                 if pkg[r]["team"] != r // C:
                     raise RuntimeError("R=1 package is not the own team")
                 dq_part[r] = pkg[r]["dq"]
+        # dK/dV (reading c11, revised): every holder of a stationary team block sends each
+        # unit's rows of its fp32 partial straight to the unit's owner, which sums the C
+        # replicas (one per team member that held the block).
+        contrib = {u: [] for u in range(P)}
         for r in range(P):
             st = stat[r]
-            net.send(1, "REV_DKV", R, r, recv[r], st["b"], 2 * C * n * E * 4, (st["dk"], st["dv"]))
-        for r in range(P):
-            b, dkv = net.recv("REV_DKV", R, send[r], r)
-            if b != r // C:
-                raise RuntimeError("reverse shuffle did not bring dK/dV to their team")
-            dkv_part[r] = dkv
+            b = st["b"]
+            for j, u in enumerate(range(b * C, b * C + C)):
+                piece = (_rows_of_member(st["dk"], j, n), _rows_of_member(st["dv"], j, n)) if compute else None
+                net.send(1, "REV_DKV", R, r, u, u, 2 * n * E * 4, piece)
+        for u in range(P):
+            for r in range(P):
+                if recv[r] // C == u // C:
+                    contrib[u].append(net.recv("REV_DKV", R, r, u)[1])
+        dkv_part = contrib
     else:
         for r in range(P):
             a = r % C
@@ -337,14 +345,11 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
                     contrib[u].append(net.recv("REV_DKV", R, r, u)[1])
         dkv_part = contrib
 
-    # Team reduce-scatter sums of dQ (and, paper regime, dK/dV).
+    # Team reduce-scatter sum of dQ.
     for r in range(P):
         t = r // C
         for j, p in enumerate(range(t * C, t * C + C)):
             net.send(1, "RS_DQ", R, r, p, p, n * E * 4, _rows_of_member(dq_part[r], j, n) if compute else None)
-            if plan["regime"] == "paper":
-                piece = (_rows_of_member(dkv_part[r][0], j, n), _rows_of_member(dkv_part[r][1], j, n)) if compute else None
-                net.send(1, "RS_DKV", R, r, p, p, 2 * n * E * 4, piece)
     dQ = np.zeros((N, h, d)) if compute else None
     dK = np.zeros((N, h, d)) if compute else None
     dV = np.zeros((N, h, d)) if compute else None
@@ -352,10 +357,7 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
         t = r // C
         members = range(t * C, t * C + C)
         dqs = [net.recv("RS_DQ", R, p, r)[1] for p in members]
-        if plan["regime"] == "paper":
-            dkvs = [net.recv("RS_DKV", R, p, r)[1] for p in members]
-        else:
-            dkvs = dkv_part[r]
+        dkvs = dkv_part[r]
         if compute:
             dQ[pos[r]] = sum(dqs)
             dK[pos[r]] = sum(x[0] for x in dkvs)

@@ -272,12 +272,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* sdd = stat + ss * 256 + 128 + hf * 64;
       mbar_wait(&bar[B_SF + ss], (ii >> 1) & 1);  // stats landed
       {
-        // convert the tile's statistics once: lse -> lse * log2(e) (+inf for query rows
-        // with no key at all, so exp2 gives 0 without a branch), D -> D / sqrt(d)
+        // convert the tile's statistics once, negated for packed FMAs:
+        // lse -> -lse * log2(e) (-inf for query rows with no key at all, so exp2 gives 0
+        // without a branch), D -> -D / sqrt(d)
         float* sst = stat + ss * 256;
         const int tc = threadIdx.x - 128;
         const float x = sst[tc];
-        sst[tc] = tc < 128 ? (x == -INFINITY ? INFINITY : x * kLog2e) : x * a.scale;
+        sst[tc] = tc < 128 ? (x == -INFINITY ? -INFINITY : -x * kLog2e) : -x * a.scale;
         named_bar_sync(2, kCompute);
       }
       mbar_wait(&bar[B_S], ii & 1);
@@ -289,12 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t rr[32];
         tmem_ld32(tl + hf * 64 + c * 32, rr);
         tmem_wait_ld();
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
         if (kind == 2) {  // diagonal tile: key r is visible to query column q iff r <= q
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int q = c * 32 + 2 * i;
-            float e0 = fast_exp2(fmaf(__uint_as_float(rr[2 * i]), a.scale_log2, -slse[q]));
-            float e1 = fast_exp2(fmaf(__uint_as_float(rr[2 * i + 1]), a.scale_log2, -slse[q + 1]));
+            const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])), sc2,
+                                   *reinterpret_cast<const float2*>(slse + q));
+            float e0 = fast_exp2(x.x), e1 = fast_exp2(x.y);
             if (hf * 64 + q < r) e0 = 0.f;
             if (hf * 64 + q + 1 < r) e1 = 0.f;
             pk[c * 16 + i] = pack_bf16x2(e0, e1);
@@ -303,8 +306,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int q = c * 32 + 2 * i;
-            pk[c * 16 + i] = pack_bf16x2(fast_exp2(fmaf(__uint_as_float(rr[2 * i]), a.scale_log2, -slse[q])),
-                                         fast_exp2(fmaf(__uint_as_float(rr[2 * i + 1]), a.scale_log2, -slse[q + 1])));
+            const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])), sc2,
+                                   *reinterpret_cast<const float2*>(slse + q));
+            pk[c * 16 + i] = pack_bf16x2(fast_exp2(x.x), fast_exp2(x.y));
           }
         }
       }
@@ -328,9 +332,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c * 16 + i]));
           const int q = c * 32 + 2 * i;
-          const float d0 = pf.x * fmaf(__uint_as_float(rr[2 * i]), a.scale, -sdd[q]);
-          const float d1 = pf.y * fmaf(__uint_as_float(rr[2 * i + 1]), a.scale, -sdd[q + 1]);
-          dk[c * 16 + i] = pack_bf16x2(d0, d1);
+          const float2 t = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
+                                 make_float2(a.scale, a.scale), *reinterpret_cast<const float2*>(sdd + q));
+          const float2 d = fmul2(pf, t);
+          dk[c * 16 + i] = pack_bf16x2(d.x, d.y);
         }
       }
       // dS -> smem (A of both dK and dQ): this half's 64 q = panel hf, row r

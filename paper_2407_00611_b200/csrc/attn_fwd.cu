@@ -292,27 +292,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           m = mnew;
         }
         const float mm = (m == -INFINITY) ? 0.f : m;
-        float rs = 0.f;
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mm, -mm);
+        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float x0 = fmaf(s[c * 32 + 2 * i], a.scale_log2, -mm);
-            const float x1 = fmaf(s[c * 32 + 2 * i + 1], a.scale_log2, -mm);
+            const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
 #if WF_POLY_EVERY > 0
             const bool poly = ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
-            const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
-            const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+            const float2 p = poly ? make_float2(poly_exp2(x.x), poly_exp2(x.y))
+                                  : make_float2(fast_exp2(x.x), fast_exp2(x.y));
 #else
-            const float p0 = fast_exp2(x0);
-            const float p1 = fast_exp2(x1);
+            const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
 #endif
-            rs += p0 + p1;
-            pk[i] = pack_bf16x2(p0, p1);
+            rs2[c] = fadd2(rs2[c], p);
+            pk[i] = pack_bf16x2(p.x, p.y);
           }
           tmem_st16(tl + cS + c * 16, pk);
         }
+        const float2 rsa = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+        const float rs = rsa.x + rsa.y;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar[B_P + 4 * t]);

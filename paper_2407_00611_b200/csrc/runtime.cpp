@@ -284,8 +284,6 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
       if (g.paper) {
         add(&b.kt, team * 2);
         add(&b.vt, team * 2);
-        add(&b.rsk, team * 4);
-        add(&b.rsv, team * 4);
       }
     }
     for (int s = 0; s < 2; ++s) {
@@ -307,14 +305,10 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
     if (g.R > 1) add(&b.home_dq, team * 4);
     add(&b.dk_acc, Bk * E * 4);
     add(&b.dv_acc, Bk * E * 4);
-    if (g.paper) {
-      if (C > 1) {
-        add(&b.rev_k, team * 4);
-        add(&b.rev_v, team * 4);
-      }
-    } else {
-      add(&b.rev_k, static_cast<int64_t>(g.T) * n * E * 4);
-      add(&b.rev_v, static_cast<int64_t>(g.T) * n * E * 4);
+    {  // dK/dV replica slots on the owner (holders of a unit: C paper, T extension)
+      const int64_t slots = g.paper ? C : g.T;
+      add(&b.rev_k, slots * n * E * 4);
+      add(&b.rev_v, slots * n * E * 4);
     }
   }
   size_t total = kFlagBytes;
@@ -921,73 +915,43 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     for (int r = 0; r < P; ++r) home[r] = pdq(r, 0);
   }
 
-  // dK/dV: reverse shuffle (paper) or straight to the unit owners (extension)
+  // dK/dV (reading c11): every holder of a stationary block sends each unit's rows of its
+  // fp32 partial straight to the unit's owner, who sums the replicas.  Holders of unit u:
+  // paper regime, the C ranks whose stationary block is team(u); extension, the T ranks
+  // whose slice contains u.  With peer memory the owner's sum kernel reads the holders'
+  // accumulators in place (pull).
+  auto first_unit = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
+  const int units_held = g.paper ? C : g.W;
   std::vector<std::vector<const float*>> kparts(P), vparts(P);
-  if (g.paper) {
+  {
+    std::vector<std::vector<int>> holders(P);
+    for (int r = 0; r < P; ++r)
+      for (int u = first_unit(r); u < first_unit(r) + units_held; ++u) holders[u].push_back(r);
+    auto slot_of = [&](int u, int r) {
+      return static_cast<int>(std::find(holders[u].begin(), holders[u].end(), r) - holders[u].begin());
+    };
     std::vector<Xfer> xs;
     for (int r = 0; r < P; ++r) {
-      const int dst = pl.recv[r];
-      if (dst == r) continue;
-      Xfer x{1, WF_KIND_REV_DKV, R, r, dst, pl.recv[r] / C, {}};
-      x.segs.push_back({lp(r, B(ctx, r).dk_acc), lp(dst, B(ctx, dst).rev_k), team * 4});
-      x.segs.push_back({lp(r, B(ctx, r).dv_acc), lp(dst, B(ctx, dst).rev_v), team * 4});
-      xs.push_back(x);
-    }
-    WCK(run_phase(ctx, xs, tr, st));
-    // replica partial of my team's block: received from init_send[r] (or my own when self)
-    std::vector<const float*> rk(P), rv(P);
-    for (int r = 0; r < P; ++r) {
-      const bool self = pl.send[r] == r;
-      rk[r] = self ? lp(r, B(ctx, r).dk_acc) : lp(r, B(ctx, r).rev_k);
-      rv[r] = self ? lp(r, B(ctx, r).dv_acc) : lp(r, B(ctx, r).rev_v);
-    }
-    if (C > 1) {
-      std::vector<Xfer> ys;
-      for (int r = 0; r < P; ++r) {
-        const int t = r / C, j = r - t * C;
-        for (int p = t * C; p < t * C + C; ++p) {
-          if (p == r) continue;
-          const int jp = p - t * C;
-          Xfer x{1, WF_KIND_RS_DKV, R, r, p, p, {}, ctx->ipc};
-          x.segs.push_back({at(rk[r], jp * n * E), at(lp(p, B(ctx, p).rsk), j * n * E), n * E * 4});
-          x.segs.push_back({at(rv[r], jp * n * E), at(lp(p, B(ctx, p).rsv), j * n * E), n * E * 4});
-          ys.push_back(x);
-        }
-      }
-      WCK(run_phase(ctx, ys, tr, st));
-    }
-    for (int r = 0; r < P; ++r) {
-      const int j = r % C;
-      for (int i = 0; i < C; ++i) {
-        const int ri = (r / C) * C + i;  // team member i holds a replica partial of my rows
-        kparts[r].push_back(i == j ? at(rk[r], i * n * E)
-                                   : ctx->ipc ? at(rk[ri], j * n * E) : at(lp(r, B(ctx, r).rsk), i * n * E));
-        vparts[r].push_back(i == j ? at(rv[r], i * n * E)
-                                   : ctx->ipc ? at(rv[ri], j * n * E) : at(lp(r, B(ctx, r).rsv), i * n * E));
-      }
-    }
-  } else {
-    std::vector<Xfer> xs;
-    for (int r = 0; r < P; ++r) {
-      const int a = r % C;
-      for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
-        const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
-        const int slot = r / C;
-        Xfer x{1, WF_KIND_REV_DKV, R, r, u, u, {}};
+      for (int u = first_unit(r); u < first_unit(r) + units_held; ++u) {
         if (u == r) continue;
-        x.segs.push_back({at(lp(r, B(ctx, r).dk_acc), o), at(lp(u, B(ctx, u).rev_k), slot * n * E), n * E * 4});
-        x.segs.push_back({at(lp(r, B(ctx, r).dv_acc), o), at(lp(u, B(ctx, u).rev_v), slot * n * E), n * E * 4});
+        const int64_t o = static_cast<int64_t>(u - first_unit(r)) * n * E;
+        const int64_t so = static_cast<int64_t>(slot_of(u, r)) * n * E;
+        Xfer x{1, WF_KIND_REV_DKV, R, r, u, u, {}, ctx->ipc};
+        x.segs.push_back({at(lp(r, B(ctx, r).dk_acc), o), at(lp(u, B(ctx, u).rev_k), so), n * E * 4});
+        x.segs.push_back({at(lp(r, B(ctx, r).dv_acc), o), at(lp(u, B(ctx, u).rev_v), so), n * E * 4});
         xs.push_back(x);
       }
     }
     WCK(run_phase(ctx, xs, tr, st));
     for (int u = 0; u < P; ++u) {
-      const int a = u / g.W;
-      for (int t = 0; t < T; ++t) {
-        const int r = t * C + a;
-        const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
-        kparts[u].push_back(r == u ? at(lp(u, B(ctx, u).dk_acc), o) : at(lp(u, B(ctx, u).rev_k), t * n * E));
-        vparts[u].push_back(r == u ? at(lp(u, B(ctx, u).dv_acc), o) : at(lp(u, B(ctx, u).rev_v), t * n * E));
+      for (size_t i = 0; i < holders[u].size(); ++i) {
+        const int r = holders[u][i];
+        const int64_t o = static_cast<int64_t>(u - first_unit(r)) * n * E;
+        const bool own = r == u;
+        kparts[u].push_back(own || ctx->ipc ? at(lp(r, B(ctx, r).dk_acc), o)
+                                            : at(lp(u, B(ctx, u).rev_k), static_cast<int64_t>(i) * n * E));
+        vparts[u].push_back(own || ctx->ipc ? at(lp(r, B(ctx, r).dv_acc), o)
+                                            : at(lp(u, B(ctx, u).rev_v), static_cast<int64_t>(i) * n * E));
       }
     }
   }
