@@ -103,7 +103,7 @@ struct wf_ctx {
   uint32_t sent[2][kMaxRanks] = {}, rcvd[2][kMaxRanks] = {};
   uint32_t acks_sent[kMaxRanks] = {}, ack_base[kMaxRanks] = {};  // monotonic across calls
   uint32_t epoch = 0;
-  std::vector<cudaEvent_t> ev_step;
+  std::vector<cudaEvent_t> ev_step, ev_src;
   cudaEvent_t ev_c = nullptr;
   // kernel timing (bench)
   bool profiling = false;
@@ -419,6 +419,57 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
   return WF_OK;
 }
 
+// Peer-memory phase whose receive side completes per source: copies and signals as in
+// run_phase, then one wait per source followed by an event, so compute that needs only
+// some sources can start before the rest have arrived (unit-pipelined R = 1 steps).
+wf_status run_phase_per_source(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& trace, cudaStream_t st,
+                               std::vector<cudaEvent_t>& src_ev) {
+  const int me = ctx->rank;
+  for (const Xfer& x : xs) {
+    if (x.src == x.dst || !recorded(ctx, x.src)) continue;
+    int64_t bytes = 0;
+    for (const Seg& sg : x.segs) bytes += sg.bytes;
+    trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
+  }
+  if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
+  const int ch = st == ctx->comm_stream ? 1 : 0;
+  cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
+  for (const Xfer& x : xs) {
+    if (x.src != me || x.pull) continue;
+    for (const Seg& sg : x.segs)
+      if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
+  }
+  SigArgs sig{}, none{};
+  bool dst_done[kMaxRanks] = {}, src_done[kMaxRanks] = {};
+  for (const Xfer& x : xs) {
+    if (x.src == me && x.dst != me && !dst_done[x.dst]) {
+      dst_done[x.dst] = true;
+      sig.dst[sig.n] = flag_of(ctx, x.dst, ch * 64 + me);
+      sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
+    }
+  }
+  CK(launch_signal_wait(sig, none, st));
+  for (const Xfer& x : xs) {
+    if (x.dst == me && x.src != me && !src_done[x.src]) {
+      src_done[x.src] = true;
+      SigArgs w{};
+      w.dst[0] = flag_of(ctx, me, ch * 64 + x.src);
+      w.val[0] = ++ctx->rcvd[ch][x.src];
+      w.n = 1;
+      CK(launch_signal_wait(none, w, st));
+      CK(cudaEventRecord(src_ev[x.src], st));
+    }
+  }
+  if (pe0) {
+    cudaEvent_t e1 = pool_event(ctx);
+    cudaEventRecord(e1, st);
+    ctx->ev_phase.push_back({xs[0].kind, {pe0, e1}});
+  }
+  return WF_OK;
+}
+
+std::vector<cudaEvent_t>& source_events(wf_ctx* ctx, int n);
+
 // pointer helpers that are null for non-local ranks
 template <typename T>
 T* at(T* base, int64_t off) {
@@ -494,6 +545,14 @@ wf_status ipc_wait_ack(wf_ctx* ctx, int from, uint32_t count, cudaStream_t st) {
   CK(launch_signal_wait(sig, wt, st));
   return WF_OK;
 }
+std::vector<cudaEvent_t>& source_events(wf_ctx* ctx, int n) {
+  while (static_cast<int>(ctx->ev_src.size()) < n) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ctx->ev_src.push_back(e);
+  }
+  return ctx->ev_src;
+}
 cudaEvent_t step_event(wf_ctx* ctx, int i) {
   while (static_cast<int>(ctx->ev_step.size()) <= i) {
     cudaEvent_t e = nullptr;
@@ -531,146 +590,218 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   auto kteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).kt) : Kin(r); };
   auto vteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).vt) : Vin(r); };
 
-  // Alg. 1 l.1: team all-gather (member-major).
-  if (C > 1) {
+  // Extension regime over peer memory (R = 1): unit-pipelined.  The team gather of Q and
+  // the K/V slice pull run on the comm stream with one completion event per source rank;
+  // the step is cut into (query unit, key unit) launches that merge into the same (O, lse)
+  // state, the locally present units first, so the transfers overlap the compute.
+  const bool unitpipe = ctx->ipc && !g.paper && C > 1;
+  if (unitpipe) {
+    const int me = ctx->rank, t = me / C, a = me % C;
+    std::vector<cudaEvent_t>& sev = source_events(ctx, P);
+    CK(cudaEventRecord(ctx->ev_a, st));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
     std::vector<Xfer> xs;
     for (int r = 0; r < P; ++r) {
-      const int t = r / C, j = r - t * C;
-      for (int p = t * C; p < t * C + C; ++p) {
+      const int tr_ = r / C, j = r - tr_ * C;
+      for (int p = tr_ * C; p < tr_ * C + C; ++p) {
+        if (p == r) continue;  // my own rows are read from the caller's buffer
         Xfer x{0, WF_KIND_AG_Q, -1, r, p, r, {}};
         x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
         xs.push_back(x);
-        if (g.paper) {
-          Xfer y{0, WF_KIND_AG_KV, -1, r, p, r, {}};
-          y.segs.push_back({Kin(r), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
-          y.segs.push_back({Vin(r), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
-          xs.push_back(y);
-        }
       }
-    }
-    WCK(run_phase(ctx, xs, tr, st));
-  }
-
-  // Per rank: pointers of the K/V block in ring slot 0/1.
-  std::vector<const bf16*> ck0(P, nullptr), cv0(P, nullptr);
-  if (g.paper) {
-    // Alg. 1 l.2: initial shuffle to init_send (a self "send" keeps the block in place).
-    std::vector<Xfer> xs;
-    for (int r = 0; r < P; ++r) {
-      const int dst = pl.send[r];
-      if (dst == r) continue;
-      Xfer x{0, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
-      x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), static_cast<int64_t>(C) * n * E * 2});
-      x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), static_cast<int64_t>(C) * n * E * 2});
-      xs.push_back(x);
-    }
-    WCK(run_phase(ctx, xs, tr, st));
-    for (int r = 0; r < P; ++r) {
-      if (pl.send[r] == r) {  // recv[r] == r too
-        ck0[r] = kteam(r);
-        cv0[r] = vteam(r);
-      } else {
-        ck0[r] = lp(r, B(ctx, r).rk[0]);
-        cv0[r] = lp(r, B(ctx, r).rv[0]);
-      }
-    }
-  } else {
-    // extension: member a pulls K/V slice a straight from the unit owners.
-    std::vector<Xfer> xs;
-    for (int r = 0; r < P; ++r) {
-      const int a = r % C;
-      for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
-        const int64_t off = static_cast<int64_t>(u - a * g.W) * n * E;
+      const int ar = r % C;
+      for (int u = ar * g.W; u < (ar + 1) * g.W; ++u) {
+        if (u == r) continue;
+        const int64_t off = static_cast<int64_t>(u - ar * g.W) * n * E;
         Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
         x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
         x.segs.push_back({Vin(u), at(lp(r, B(ctx, r).rv[0]), off), n * E * 2});
         xs.push_back(x);
       }
     }
-    WCK(run_phase(ctx, xs, tr, st));
-    for (int r = 0; r < P; ++r) {
-      ck0[r] = lp(r, B(ctx, r).rk[0]);
-      cv0[r] = lp(r, B(ctx, r).rv[0]);
+    WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    RankBufs& b = B(ctx, me);
+    std::vector<int> qorder, korder;
+    for (int i = 0; i < C; ++i) qorder.push_back(t * C + (a + i) % C);  // own unit first
+    for (int i = 0; i < g.W; ++i) {
+      const int u = a * g.W + i;
+      if (u == me) korder.insert(korder.begin(), u); else korder.push_back(u);
     }
-  }
-
-  // Alg. 1 l.5-10: R ring steps, K/V double buffered; the transfer of block s+1
-  // (comm stream) is posted before the block kernel of step s.
-  const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
-  auto slot_k = [&](int r, int s) -> const bf16* { return s == 0 ? ck0[r] : lp(r, B(ctx, r).rk[s & 1]); };
-  auto slot_v = [&](int r, int s) -> const bf16* { return s == 0 ? cv0[r] : lp(r, B(ctx, r).rv[s & 1]); };
-  auto compute = [&](int r, int s) -> wf_status {
-    RankBufs& b = B(ctx, r);
-    FwdArgs a{};
-    a.nq = C * g.n;
-    a.nk = g.Bk;
-    a.heads = g.h;
-    a.causal = g.causal;
-    a.qpos = units_table(g, (r / C) * C, C);
-    a.kpos = g.paper ? units_table(g, pl.block_at(r, s) * C, C) : units_table(g, (r % C) * g.W, g.W);
-    a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(g.d));
-    a.o_in = s > 0 ? b.o_state : nullptr;
-    a.lse_in = s > 0 ? b.lse_state : nullptr;
-    a.lse_blk = g.n;
-    if (s < R - 1) {  // intermediate step: fp32 (O, lse) state, merged in place next step
-      a.o_out_f32 = b.o_state;
-      a.lse_out = b.lse_state;
-    } else if (C == 1) {  // final output
-      a.o_out_bf16 = Oout(r);
-      a.lse_out = Lout(r);
-    } else {  // this member's fp32 partial for the team rows (reading c17)
-      a.o_out_f32 = b.o_state;
-      a.lse_out = b.lse_state;
+    for (int qj : qorder) {
+      const int jm = qj - t * C;
+      const bf16* qp = qj == me ? Qin(me) : b.qt + jm * n * E;
+      for (size_t ki = 0; ki < korder.size(); ++ki) {
+        const int u = korder[ki];
+        const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
+        const bf16* kp = u == me ? Kin(me) : b.rk[0] + koff;
+        const bf16* vp = u == me ? Vin(me) : b.rv[0] + koff;
+        if (qj != me) CK(cudaStreamWaitEvent(st, sev[qj], 0));
+        if (u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
+        FwdArgs fa{};
+        fa.nq = g.n;
+        fa.nk = g.n;
+        fa.heads = g.h;
+        fa.causal = g.causal;
+        fa.qpos = units_table(g, qj, 1);
+        fa.kpos = units_table(g, u, 1);
+        fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(g.d));
+        fa.o_in = ki > 0 ? b.o_state + jm * n * E : nullptr;
+        fa.lse_in = ki > 0 ? b.lse_state + jm * h * n : nullptr;
+        fa.o_out_f32 = b.o_state + jm * n * E;
+        fa.lse_out = b.lse_state + jm * h * n;
+        fa.lse_blk = g.n;
+        CUtensorMap tq, tk, tv;
+        if (!make_tmap_rows(&tq, qp, fa.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, fa.nk, g.h, g.d) ||
+            !make_tmap_rows(&tv, vp, fa.nk, g.h, g.d))
+          return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        cudaEvent_t e0 = prof_begin(ctx, st);
+        WCK(kcheck(ctx, launch_block_fwd(tq, tk, tv, fa, g.d, st), "block_fwd"));
+        prof_end(ctx, st, e0, ctx->ev_fwd);
+      }
     }
-    if (ctx->dry) return WF_OK;
-    CUtensorMap tq, tk, tv;
-    if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
-        !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
-      return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
-    cudaEvent_t e0 = prof_begin(ctx, st);
-    wf_status ks = kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
-    prof_end(ctx, st, e0, ctx->ev_fwd);
-    return ks;
-  };
-  if (overlap) CK(cudaEventRecord(ctx->ev_a, st));  // slot 0 ready
-  for (int s = 0; s < R; ++s) {
-    std::vector<Xfer> xs;
-    if (s < R - 1) {
+  } else {
+    // Alg. 1 l.1: team all-gather (member-major).
+    if (C > 1) {
+      std::vector<Xfer> xs;
       for (int r = 0; r < P; ++r) {
-        const int dst = pl.next[r];
-        Xfer x{0, WF_KIND_RING_KV, s, r, dst, g.paper ? pl.block_at(r, s) : r, {}};
-        x.segs.push_back({slot_k(r, s), lp(dst, B(ctx, dst).rk[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
-        x.segs.push_back({slot_v(r, s), lp(dst, B(ctx, dst).rv[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
+        const int t = r / C, j = r - t * C;
+        for (int p = t * C; p < t * C + C; ++p) {
+          Xfer x{0, WF_KIND_AG_Q, -1, r, p, r, {}};
+          x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+          xs.push_back(x);
+          if (g.paper) {
+            Xfer y{0, WF_KIND_AG_KV, -1, r, p, r, {}};
+            y.segs.push_back({Kin(r), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
+            y.segs.push_back({Vin(r), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
+            xs.push_back(y);
+          }
+        }
+      }
+      WCK(run_phase(ctx, xs, tr, st));
+    }
+
+    // Per rank: pointers of the K/V block in ring slot 0/1.
+    std::vector<const bf16*> ck0(P, nullptr), cv0(P, nullptr);
+    if (g.paper) {
+      // Alg. 1 l.2: initial shuffle to init_send (a self "send" keeps the block in place).
+      std::vector<Xfer> xs;
+      for (int r = 0; r < P; ++r) {
+        const int dst = pl.send[r];
+        if (dst == r) continue;
+        Xfer x{0, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
+        x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), static_cast<int64_t>(C) * n * E * 2});
+        x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), static_cast<int64_t>(C) * n * E * 2});
         xs.push_back(x);
       }
-      if (overlap && ctx->ipc) {
-        // Alg. 1 l.8 with peer copies: the comm stream pushes block s into next's other
-        // slot as soon as next has released it (its step s-1), independent of my compute.
-        if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-        WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
-        WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
-        CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
-      } else if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
-        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-        WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
-        CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+      WCK(run_phase(ctx, xs, tr, st));
+      for (int r = 0; r < P; ++r) {
+        if (pl.send[r] == r) {  // recv[r] == r too
+          ck0[r] = kteam(r);
+          cv0[r] = vteam(r);
+        } else {
+          ck0[r] = lp(r, B(ctx, r).rk[0]);
+          cv0[r] = lp(r, B(ctx, r).rv[0]);
+        }
+      }
+    } else {
+      // extension: member a pulls K/V slice a straight from the unit owners.
+      std::vector<Xfer> xs;
+      for (int r = 0; r < P; ++r) {
+        const int a = r % C;
+        for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
+          const int64_t off = static_cast<int64_t>(u - a * g.W) * n * E;
+          Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+          x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
+          x.segs.push_back({Vin(u), at(lp(r, B(ctx, r).rv[0]), off), n * E * 2});
+          xs.push_back(x);
+        }
+      }
+      WCK(run_phase(ctx, xs, tr, st));
+      for (int r = 0; r < P; ++r) {
+        ck0[r] = lp(r, B(ctx, r).rk[0]);
+        cv0[r] = lp(r, B(ctx, r).rv[0]);
       }
     }
-    for (int r = 0; r < P; ++r)
-      if (local(ctx, r)) WCK(compute(r, s));
-    if (s < R - 1) {
-      if (overlap && ctx->ipc) {
-        WCK(ipc_ack(ctx, pl.last[ctx->rank], st));  // my slot s is free again
-        CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
-      } else if (overlap) {
-        CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
-        CK(cudaEventRecord(ctx->ev_a, st));
-      } else {
-        WCK(run_phase(ctx, xs, tr, st));
+
+    // Alg. 1 l.5-10: R ring steps, K/V double buffered; the transfer of block s+1
+    // (comm stream) is posted before the block kernel of step s.
+    const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
+    auto slot_k = [&](int r, int s) -> const bf16* { return s == 0 ? ck0[r] : lp(r, B(ctx, r).rk[s & 1]); };
+    auto slot_v = [&](int r, int s) -> const bf16* { return s == 0 ? cv0[r] : lp(r, B(ctx, r).rv[s & 1]); };
+    auto compute = [&](int r, int s) -> wf_status {
+      RankBufs& b = B(ctx, r);
+      FwdArgs a{};
+      a.nq = C * g.n;
+      a.nk = g.Bk;
+      a.heads = g.h;
+      a.causal = g.causal;
+      a.qpos = units_table(g, (r / C) * C, C);
+      a.kpos = g.paper ? units_table(g, pl.block_at(r, s) * C, C) : units_table(g, (r % C) * g.W, g.W);
+      a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(g.d));
+      a.o_in = s > 0 ? b.o_state : nullptr;
+      a.lse_in = s > 0 ? b.lse_state : nullptr;
+      a.lse_blk = g.n;
+      if (s < R - 1) {  // intermediate step: fp32 (O, lse) state, merged in place next step
+        a.o_out_f32 = b.o_state;
+        a.lse_out = b.lse_state;
+      } else if (C == 1) {  // final output
+        a.o_out_bf16 = Oout(r);
+        a.lse_out = Lout(r);
+      } else {  // this member's fp32 partial for the team rows (reading c17)
+        a.o_out_f32 = b.o_state;
+        a.lse_out = b.lse_state;
+      }
+      if (ctx->dry) return WF_OK;
+      CUtensorMap tq, tk, tv;
+      if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
+          !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
+        return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+      cudaEvent_t e0 = prof_begin(ctx, st);
+      wf_status ks = kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
+      prof_end(ctx, st, e0, ctx->ev_fwd);
+      return ks;
+    };
+    if (overlap) CK(cudaEventRecord(ctx->ev_a, st));  // slot 0 ready
+    for (int s = 0; s < R; ++s) {
+      std::vector<Xfer> xs;
+      if (s < R - 1) {
+        for (int r = 0; r < P; ++r) {
+          const int dst = pl.next[r];
+          Xfer x{0, WF_KIND_RING_KV, s, r, dst, g.paper ? pl.block_at(r, s) : r, {}};
+          x.segs.push_back({slot_k(r, s), lp(dst, B(ctx, dst).rk[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
+          x.segs.push_back({slot_v(r, s), lp(dst, B(ctx, dst).rv[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
+          xs.push_back(x);
+        }
+        if (overlap && ctx->ipc) {
+          // Alg. 1 l.8 with peer copies: the comm stream pushes block s into next's other
+          // slot as soon as next has released it (its step s-1), independent of my compute.
+          if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+          WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
+          WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
+          CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
+        } else if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
+          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+          WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
+          CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+        }
+      }
+      for (int r = 0; r < P; ++r)
+        if (local(ctx, r)) WCK(compute(r, s));
+      if (s < R - 1) {
+        if (overlap && ctx->ipc) {
+          WCK(ipc_ack(ctx, pl.last[ctx->rank], st));  // my slot s is free again
+          CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
+        } else if (overlap) {
+          CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
+          CK(cudaEventRecord(ctx->ev_a, st));
+        } else {
+          WCK(run_phase(ctx, xs, tr, st));
+        }
       }
     }
+    if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
+
   }
-  if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
 
   // Alg. 1 l.11: ReduceScatter_combine -- partial rows to their owner, LSE-merge there.
   if (C > 1) {
@@ -747,62 +878,6 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto kteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).kt) : L(r, K, n * E); };
   auto vteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).vt) : L(r, V, n * E); };
 
-  // team gathers: Q + dO, LSE + D, and (paper regime) K + V
-  if (C > 1) {
-    std::vector<Xfer> xs;
-    for (int r = 0; r < P; ++r) {
-      const int t = r / C, j = r - t * C;
-      for (int p = t * C; p < t * C + C; ++p) {
-        Xfer x{1, WF_KIND_AG_QDO, -1, r, p, r, {}};
-        x.segs.push_back({L(r, Q, n * E), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
-        x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
-        xs.push_back(x);
-        Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
-        y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
-        y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
-        xs.push_back(y);
-        if (g.paper) {
-          Xfer z{1, WF_KIND_AG_KV, -1, r, p, r, {}};
-          z.segs.push_back({L(r, K, n * E), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
-          z.segs.push_back({L(r, V, n * E), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
-          xs.push_back(z);
-        }
-      }
-    }
-    WCK(run_phase(ctx, xs, tr, st));
-  }
-
-  // stationary K/V block: the init-shuffle block (paper) or the slice (extension)
-  std::vector<const bf16*> sk(P, nullptr), sv(P, nullptr);
-  {
-    std::vector<Xfer> xs;
-    for (int r = 0; r < P; ++r) {
-      if (g.paper) {
-        const int dst = pl.send[r];
-        if (dst == r) continue;
-        Xfer x{1, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
-        x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), team * 2});
-        x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), team * 2});
-        xs.push_back(x);
-      } else {
-        const int a = r % C;
-        for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
-          const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
-          Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
-          x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
-          x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
-          xs.push_back(x);
-        }
-      }
-    }
-    WCK(run_phase(ctx, xs, tr, st));
-    for (int r = 0; r < P; ++r) {
-      const bool self = g.paper && pl.send[r] == r;
-      sk[r] = self ? kteam(r) : lp(r, B(ctx, r).rk[0]);
-      sv[r] = self ? vteam(r) : lp(r, B(ctx, r).rv[0]);
-    }
-  }
-
   // package slots: step 0 = own team (aliases); later steps in the receive buffers
   auto pq = [&](int r, int s) -> const bf16* { return s == 0 ? qteam(r) : lp(r, B(ctx, r).pq[s & 1]); };
   auto pdo = [&](int r, int s) -> const bf16* { return s == 0 ? doteam(r) : lp(r, B(ctx, r).pdo[s & 1]); };
@@ -811,93 +886,234 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto pdq = [&](int r, int s) -> float* { return lp(r, B(ctx, r).pdq[s & 1]); };
   std::vector<int> pkg_team(P);
   for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
-  for (int r = 0; r < P; ++r)
-    if (local(ctx, r) && !ctx->dry) CK(cudaMemsetAsync(pdq(r, 0), 0, team * 4, st));
-
-  const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
-  if (overlap) CK(cudaEventRecord(ctx->ev_a, st));
-  for (int s = 0; s < R; ++s) {
-    std::vector<Xfer> pk, dq;
-    if (s < R - 1) {
-      for (int r = 0; r < P; ++r) {
-        const int dst = pl.next[r];
-        const int s1 = (s + 1) & 1;
-        Xfer x{1, WF_KIND_RING_QPKG, s, r, dst, pkg_team[r], {}};
-        x.segs.push_back({pq(r, s), lp(dst, B(ctx, dst).pq[s1]), team * 2});
-        x.segs.push_back({pdo(r, s), lp(dst, B(ctx, dst).pdo[s1]), team * 2});
-        x.segs.push_back({plse(r, s), lp(dst, B(ctx, dst).plse[s1]), C * h * n * 4});
-        x.segs.push_back({pds(r, s), lp(dst, B(ctx, dst).pdsum[s1]), C * h * n * 4});
-        pk.push_back(x);
-        Xfer y{1, WF_KIND_RING_DQ, s, r, dst, pkg_team[r], {}};
-        y.segs.push_back({pdq(r, s), lp(dst, B(ctx, dst).pdq[s1]), team * 4});
-        dq.push_back(y);
-      }
-      if (overlap && ctx->ipc) {
-        // the package does not depend on step s: push it as soon as next released the slot
-        if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-        WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
-        WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
-      } else if (overlap) {  // the package does not depend on step s: post it first
-        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-        WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
-      }
-    }
+  const bool unitpipe = ctx->ipc && !g.paper && C > 1;
+  if (unitpipe) {
+    // Extension regime over peer memory (R = 1): unit-pipelined like the forward.  The
+    // gathers of Q, dO, LSE, D and the K/V slice pull run on the comm stream with one
+    // completion event per source rank; the step is cut into (query unit, key unit)
+    // launches, locally present units first.  dQ rows accumulate per query unit, dK/dV
+    // rows per key unit.
+    const int me = ctx->rank, t = me / C, a = me % C;
+    std::vector<cudaEvent_t>& sev = source_events(ctx, P);
+    CK(cudaEventRecord(ctx->ev_a, st));  // after D of my rows
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+    std::vector<Xfer> xs;
     for (int r = 0; r < P; ++r) {
-      if (!local(ctx, r)) continue;
-      RankBufs& b = B(ctx, r);
-      BwdArgs a{};
-      a.nq = C * g.n;
-      a.nk = g.Bk;
-      a.heads = g.h;
-      a.causal = g.causal;
-      a.qpos = units_table(g, pkg_team[r] * C, C);
-      a.kpos = g.paper ? units_table(g, (pl.recv[r] / C) * C, C) : units_table(g, (r % C) * g.W, g.W);
-      a.scale = 1.f / std::sqrt(static_cast<float>(g.d));
-      a.scale_log2 = 1.4426950408889634f * a.scale;
-      a.lse = plse(r, s);
-      a.dsum = pds(r, s);
-      a.stat_blk = g.n;
-      a.dq_acc = pdq(r, s);
-      a.dk_acc = b.dk_acc;
-      a.dv_acc = b.dv_acc;
-      a.dkv_accumulate = s > 0;
-      if (ctx->dry) continue;
-      CUtensorMap tq, tk, tv, tdo;
-      if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
-          !make_tmap_rows(&tv, sv[r], a.nk, g.h, g.d) || !make_tmap_rows(&tdo, pdo(r, s), a.nq, g.h, g.d))
-        return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
-      cudaEvent_t e0 = prof_begin(ctx, st);
-      WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, a, g.d, st), "block_bwd"));
-      prof_end(ctx, st, e0, ctx->ev_bwd);
-    }
-    if (s < R - 1) {
-      if (overlap && ctx->ipc) {
-        // dQ depends on step s: push it after the step, then release my slot
-        CK(cudaEventRecord(ctx->ev_b, st));
-        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
-        WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
-        CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
-        WCK(ipc_ack(ctx, pl.last[ctx->rank], st));
-        CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
-      } else if (overlap) {
-        // dQ depends on step s: after it; the receiver's next step waits for both
-        CK(cudaEventRecord(ctx->ev_b, st));
-        CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
-        WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
-        CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
-        CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
-        CK(cudaEventRecord(ctx->ev_a, st));
-      } else {
-        WCK(run_phase(ctx, pk, tr, st));
-        WCK(run_phase(ctx, dq, tr, st));
+      const int tr_ = r / C, j = r - tr_ * C;
+      for (int p = tr_ * C; p < tr_ * C + C; ++p) {
+        if (p == r) continue;
+        Xfer x{1, WF_KIND_AG_QDO, -1, r, p, r, {}};
+        x.segs.push_back({L(r, Q, n * E), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+        x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
+        xs.push_back(x);
+        Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
+        y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
+        y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
+        xs.push_back(y);
       }
-      std::vector<int> nt(P);
-      for (int r = 0; r < P; ++r) nt[pl.next[r]] = pkg_team[r];
-      pkg_team = nt;
+      const int ar = r % C;
+      for (int u = ar * g.W; u < (ar + 1) * g.W; ++u) {
+        if (u == r) continue;
+        const int64_t o = static_cast<int64_t>(u - ar * g.W) * n * E;
+        Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+        x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
+        x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
+        xs.push_back(x);
+      }
     }
-  }
+    WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    RankBufs& b = B(ctx, me);
+    CK(cudaMemsetAsync(b.pdq[0], 0, team * 4, st));
+    std::vector<int> qorder, korder;
+    for (int i = 0; i < C; ++i) qorder.push_back(t * C + (a + i) % C);
+    for (int i = 0; i < g.W; ++i) {
+      const int u = a * g.W + i;
+      if (u == me) korder.insert(korder.begin(), u); else korder.push_back(u);
+    }
+    for (size_t qi = 0; qi < qorder.size(); ++qi) {
+      const int qj = qorder[qi];
+      const int jm = qj - t * C;
+      const bool own = qj == me;
+      const bf16* qp = own ? L(me, Q, n * E) : b.qt + jm * n * E;
+      const bf16* dop = own ? L(me, dO, n * E) : b.t_do + jm * n * E;
+      for (size_t ki = 0; ki < korder.size(); ++ki) {
+        const int u = korder[ki];
+        const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
+        const bf16* kp = u == me ? L(me, K, n * E) : b.rk[0] + koff;
+        const bf16* vp = u == me ? L(me, V, n * E) : b.rv[0] + koff;
+        if (!own) CK(cudaStreamWaitEvent(st, sev[qj], 0));
+        if (u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
+        BwdArgs ba{};
+        ba.nq = g.n;
+        ba.nk = g.n;
+        ba.heads = g.h;
+        ba.causal = g.causal;
+        ba.qpos = units_table(g, qj, 1);
+        ba.kpos = units_table(g, u, 1);
+        ba.scale = 1.f / std::sqrt(static_cast<float>(g.d));
+        ba.scale_log2 = 1.4426950408889634f * ba.scale;
+        ba.lse = own ? L(me, LSE, n * h) : b.t_lse + jm * h * n;
+        ba.dsum = own ? b.dsum : b.t_dsum + jm * h * n;
+        ba.stat_blk = g.n;
+        ba.dq_acc = b.pdq[0] + jm * n * E;
+        ba.dk_acc = b.dk_acc + koff;
+        ba.dv_acc = b.dv_acc + koff;
+        ba.dkv_accumulate = qi > 0;
+        CUtensorMap tq, tk, tv, tdo;
+        if (!make_tmap_rows(&tq, qp, ba.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, ba.nk, g.h, g.d) ||
+            !make_tmap_rows(&tv, vp, ba.nk, g.h, g.d) || !make_tmap_rows(&tdo, dop, ba.nq, g.h, g.d))
+          return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        cudaEvent_t e0 = prof_begin(ctx, st);
+        WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, ba, g.d, st), "block_bwd"));
+        prof_end(ctx, st, e0, ctx->ev_bwd);
+      }
+    }
+  } else {
+    // team gathers: Q + dO, LSE + D, and (paper regime) K + V
+    if (C > 1) {
+      std::vector<Xfer> xs;
+      for (int r = 0; r < P; ++r) {
+        const int t = r / C, j = r - t * C;
+        for (int p = t * C; p < t * C + C; ++p) {
+          Xfer x{1, WF_KIND_AG_QDO, -1, r, p, r, {}};
+          x.segs.push_back({L(r, Q, n * E), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+          x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
+          xs.push_back(x);
+          Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
+          y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
+          y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
+          xs.push_back(y);
+          if (g.paper) {
+            Xfer z{1, WF_KIND_AG_KV, -1, r, p, r, {}};
+            z.segs.push_back({L(r, K, n * E), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
+            z.segs.push_back({L(r, V, n * E), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
+            xs.push_back(z);
+          }
+        }
+      }
+      WCK(run_phase(ctx, xs, tr, st));
+    }
 
-  if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
+    // stationary K/V block: the init-shuffle block (paper) or the slice (extension)
+    std::vector<const bf16*> sk(P, nullptr), sv(P, nullptr);
+    {
+      std::vector<Xfer> xs;
+      for (int r = 0; r < P; ++r) {
+        if (g.paper) {
+          const int dst = pl.send[r];
+          if (dst == r) continue;
+          Xfer x{1, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
+          x.segs.push_back({kteam(r), lp(dst, B(ctx, dst).rk[0]), team * 2});
+          x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), team * 2});
+          xs.push_back(x);
+        } else {
+          const int a = r % C;
+          for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
+            const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
+            Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+            x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
+            x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
+            xs.push_back(x);
+          }
+        }
+      }
+      WCK(run_phase(ctx, xs, tr, st));
+      for (int r = 0; r < P; ++r) {
+        const bool self = g.paper && pl.send[r] == r;
+        sk[r] = self ? kteam(r) : lp(r, B(ctx, r).rk[0]);
+        sv[r] = self ? vteam(r) : lp(r, B(ctx, r).rv[0]);
+      }
+    }
+
+    for (int r = 0; r < P; ++r)
+      if (local(ctx, r) && !ctx->dry) CK(cudaMemsetAsync(pdq(r, 0), 0, team * 4, st));
+
+    const bool overlap = !ctx->emulated && !ctx->dry && R > 1;
+    if (overlap) CK(cudaEventRecord(ctx->ev_a, st));
+    for (int s = 0; s < R; ++s) {
+      std::vector<Xfer> pk, dq;
+      if (s < R - 1) {
+        for (int r = 0; r < P; ++r) {
+          const int dst = pl.next[r];
+          const int s1 = (s + 1) & 1;
+          Xfer x{1, WF_KIND_RING_QPKG, s, r, dst, pkg_team[r], {}};
+          x.segs.push_back({pq(r, s), lp(dst, B(ctx, dst).pq[s1]), team * 2});
+          x.segs.push_back({pdo(r, s), lp(dst, B(ctx, dst).pdo[s1]), team * 2});
+          x.segs.push_back({plse(r, s), lp(dst, B(ctx, dst).plse[s1]), C * h * n * 4});
+          x.segs.push_back({pds(r, s), lp(dst, B(ctx, dst).pdsum[s1]), C * h * n * 4});
+          pk.push_back(x);
+          Xfer y{1, WF_KIND_RING_DQ, s, r, dst, pkg_team[r], {}};
+          y.segs.push_back({pdq(r, s), lp(dst, B(ctx, dst).pdq[s1]), team * 4});
+          dq.push_back(y);
+        }
+        if (overlap && ctx->ipc) {
+          // the package does not depend on step s: push it as soon as next released the slot
+          if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+          WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
+          WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
+        } else if (overlap) {  // the package does not depend on step s: post it first
+          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
+          WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
+        }
+      }
+      for (int r = 0; r < P; ++r) {
+        if (!local(ctx, r)) continue;
+        RankBufs& b = B(ctx, r);
+        BwdArgs a{};
+        a.nq = C * g.n;
+        a.nk = g.Bk;
+        a.heads = g.h;
+        a.causal = g.causal;
+        a.qpos = units_table(g, pkg_team[r] * C, C);
+        a.kpos = g.paper ? units_table(g, (pl.recv[r] / C) * C, C) : units_table(g, (r % C) * g.W, g.W);
+        a.scale = 1.f / std::sqrt(static_cast<float>(g.d));
+        a.scale_log2 = 1.4426950408889634f * a.scale;
+        a.lse = plse(r, s);
+        a.dsum = pds(r, s);
+        a.stat_blk = g.n;
+        a.dq_acc = pdq(r, s);
+        a.dk_acc = b.dk_acc;
+        a.dv_acc = b.dv_acc;
+        a.dkv_accumulate = s > 0;
+        if (ctx->dry) continue;
+        CUtensorMap tq, tk, tv, tdo;
+        if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
+            !make_tmap_rows(&tv, sv[r], a.nk, g.h, g.d) || !make_tmap_rows(&tdo, pdo(r, s), a.nq, g.h, g.d))
+          return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        cudaEvent_t e0 = prof_begin(ctx, st);
+        WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, a, g.d, st), "block_bwd"));
+        prof_end(ctx, st, e0, ctx->ev_bwd);
+      }
+      if (s < R - 1) {
+        if (overlap && ctx->ipc) {
+          // dQ depends on step s: push it after the step, then release my slot
+          CK(cudaEventRecord(ctx->ev_b, st));
+          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+          WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
+          CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
+          WCK(ipc_ack(ctx, pl.last[ctx->rank], st));
+          CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
+        } else if (overlap) {
+          // dQ depends on step s: after it; the receiver's next step waits for both
+          CK(cudaEventRecord(ctx->ev_b, st));
+          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+          WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
+          CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
+          CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
+          CK(cudaEventRecord(ctx->ev_a, st));
+        } else {
+          WCK(run_phase(ctx, pk, tr, st));
+          WCK(run_phase(ctx, dq, tr, st));
+        }
+        std::vector<int> nt(P);
+        for (int r = 0; r < P; ++r) nt[pl.next[r]] = pkg_team[r];
+        pkg_team = nt;
+      }
+    }
+
+    if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
+
+  }
 
   // return hop: dQ back to its home
   std::vector<float*> home(P, nullptr);
@@ -1250,6 +1466,7 @@ wf_status wf_finalize(wf_ctx* ctx) {
     cudaFree(ctx->ws);
   }
   for (cudaEvent_t e : ctx->ev_step) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_src) cudaEventDestroy(e);
   if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
