@@ -55,6 +55,9 @@ enum {
   B_DS = 16, B_DQF = 17, B_DQE = 18, B_DSE = 19, B_DONE = 20, B_NUM = 21
 };
 
+#ifndef WF_DQ_ATOMIC
+#define WF_DQ_ATOMIC 0
+#endif
 constexpr int kThreads = 14 * 32;  // 4 dQ-drain + 8 compute + TMA + MMA warps
 constexpr int kCompute = 256;
 
@@ -461,6 +464,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (sub == 1 && !two) break;
             const int c0 = cbase + 32 * sub;
             const uint32_t* rr = sub == 0 ? ra : rb;
+#if WF_DQ_ATOMIC
+            // experiment: vector reductions straight from registers (no shared memory)
+            float* dst = a.dq_acc + (static_cast<size_t>(it * WF_TILE + r) * a.heads + head) * D + c0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (c0 + 4 * j < D)
+                atomicAdd(reinterpret_cast<float4*>(dst) + j,
+                          make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                      __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3])));
+            (void)wbox0;
+#else
             uint8_t* wbox = wbox0 + (chunk & 1) * 4096;
             if (lane == 0) bulk_wait_read<1>();  // the reduce of chunk-2 has read this box
             __syncwarp();
@@ -474,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_reduce_add_3d(&tmDQ, wbox, c0, head, it * WF_TILE + warp * 32);
               bulk_commit();
             }
+#endif
             ++chunk;
           }
         }

@@ -268,9 +268,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int c = 0; c < 128; ++c)
             if (kind == 0 || c > row) s[c] = -INFINITY;
         }
-        float mx = s[0];
+        // row max as 8 independent chains (3-input FMNMX), then a small tree: a single
+        // 128-long dependent chain would cost ~500 cycles of latency per tile
+        float mxs[8];
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(s[k], s[8 + k]);
+#pragma unroll
+        for (int c = 16; c < 128; c += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(mxs[k], fmaxf(s[c + k], s[c + 8 + k]));
+        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
         const float mcand = mx * a.scale_log2;
         const bool need = mcand > m + 8.0f;
         if (__any_sync(0xffffffffu, need)) {
@@ -302,8 +310,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
 #if WF_POLY_EVERY > 0
             const bool poly = ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
-            const float2 p = poly ? make_float2(poly_exp2(x.x), poly_exp2(x.y))
-                                  : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            const float2 p = poly ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
 #else
             const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
 #endif

@@ -234,6 +234,21 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return d;
 }
 
+// Two exponentials on the FMA pipe with packed fp32x2 arithmetic (same polynomial as
+// poly_exp2): 6 FP32x2 + 4 integer instructions for the pair, no MUFU.
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 f = fadd2(x, fadd2(magic, make_float2(-t.x, -t.y)));
+  float2 p = ffma2(make_float2(0.05502927f, 0.05502927f), f, make_float2(0.24225698f, 0.24225698f));
+  p = ffma2(p, f, make_float2(0.69325305f, 0.69325305f));
+  p = ffma2(p, f, make_float2(0.99995134f, 0.99995134f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

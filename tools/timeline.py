@@ -1,6 +1,7 @@
 """Record the block kernels' warp-role timelines (clock64 stamps of one CTA) at the
 bench workload and save them to gpurun_out/timeline_{fwd,bwd}.npy (GPU box helper)."""
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -27,6 +28,6 @@ for name in ("fwd", "bwd"):
         ctx.bwd(do, q, k, v, o, lse, N, True, dq=dq, dk=dk, dv=dv)
     buf = (ctypes.c_uint64 * n)()
     assert lib().wf_debug_timeline_read(buf, n) == 0
-    np.save(f"gpurun_out/timeline_{name}.npy", np.frombuffer(buf, dtype=np.uint64).reshape(4, 1024, 8))
+    np.save(f"gpurun_out/timeline_{name}{os.environ.get('TLTAG', '')}.npy", np.frombuffer(buf, dtype=np.uint64).reshape(4, 1024, 8))
     lib().wf_debug_timeline(-1)
 print("saved")

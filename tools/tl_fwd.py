@@ -8,5 +8,5 @@ print('MMA: start->PV0 issued',med(t[0,:n,1]-t[0,:n,0]),'->S0 issued',med(t[0,:n
 for r in (1,2):
     sm=t[r,:n,1]-t[r,:n,0]; w=np.r_[t[r,1:n,0]-t[r,:n-1,1],0]
     print('softmax WG',r-1,'phase',med(sm),'wait next S',med(w))
-print('TMA K issue -> S0 issue', med(t[0,:n,2]-t[3,:n,0]))
+#print('TMA K issue -> S0 issue', med(t[0,:n,2]-t[3,:n,0]))
 for j in range(100,103): print(j, t[0,j,:5], t[1,j,:2], t[2,j,:2], t[3,j,0])
