@@ -255,7 +255,15 @@ def main():
         t_nocomm = float(tn.item())
         exposed = {"frac": max(0.0, (ms - t_nocomm) / ms), "ms_per_step_no_transfer": t_nocomm / args.steps}
 
-    # roofline of the dominant kernel (the block backward: 5 of the 7 GEMM-equivalents)
+    # roofline of the dominant kernel (the block backward: 5 of the 7 GEMM-equivalents);
+    # its DRAM traffic per launch comes from the committed ncu capture of the same workload
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r01_kernels.json")))
+        key = f"{args.workload}{N // 1024}k_{'causal' if causal else 'full'}_{heads}x{hd}_p{P}"
+        traffic = prof.get(key, {}).get("wf_block_bwd_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     peaks = load_peaks()
     peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
     per_gpu_f, per_gpu_b = ff / P, fb / P
@@ -304,7 +312,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        N_s = 16384
+        N_s = 24576
         v_cpu, dt, cores = cpu_oracle_sample(N_s, 1, hd, causal)
         cpu = {"value": v_cpu, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                "sample": f"dense fp64 fwd+bwd, 1 of {heads} heads, N={N_s} of {N} tokens ({dt:.1f} s)"}
@@ -322,7 +330,7 @@ def main():
             "fwd_kernel_tflops": achieved_f, "bwd_kernel_tflops": achieved_b,
             "kernel_ms_per_step": {"block_fwd": fwd_ms / args.steps, "block_bwd": bwd_ms / args.steps},
             "roofline": {"kernel": "wf_block_bwd_kernel", "bound": "tensor", "achieved": achieved_b, "peak": peak,
-                         "unit": "TFLOP/s", "frac": (achieved_b / peak) if achieved_b else None, "traffic": None,
+                         "unit": "TFLOP/s", "frac": (achieved_b / peak) if achieved_b else None, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                          "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
             "exposed_comm": exposed,
