@@ -310,6 +310,16 @@ def main():
         e2e = {"value": (ff + fb) * steps_e / (el / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": el / steps_e}
 
+    # analytic model (costmodel.py, Eqs. 2-7) fed with this run's kernel rates
+    model = None
+    if achieved_f and achieved_b:
+        from paper_2407_00611_b200 import costmodel
+        pr = costmodel.predict(P, C, N, heads, hd, causal, achieved_f, achieved_b)
+        mem = costmodel.memory(P, C, N, heads, hd, causal)
+        model = {"pred_ms_per_step": pr["total_ms"], "pred_exposed_frac": pr["exposed_comm_frac"],
+                 "link_gbps_assumed": 700.0, "recv_bytes_per_rank": pr["recv_bytes_max"],
+                 "workspace_bytes": mem["workspace_bytes"], "workspace_over_A": mem["workspace_over_A"]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         N_s = 24576
@@ -334,6 +344,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                          "frac_of_burst": (achieved_b / peaks.get("bf16_tflops", peak)) if achieved_b else None},
             "exposed_comm": exposed,
+            "cost_model": model,
             "scheduler": sched,
             "phase_ms_per_step": phase_ms,
             "cpu_baseline": cpu,

@@ -110,6 +110,13 @@ wf_status wf_get_trace(wf_ctx* ctx, wf_event* buf, size_t cap, size_t* n_out);
 wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,
                         size_t* n_out);
 
+/* Host-only: bytes of device workspace one rank of a (P, C) context allocates for this
+ * shape (team buffers, double-buffered ring slots, fp32 accumulators and dK/dV replica
+ * slots).  This is the library's counterpart of the paper's 3CA activation
+ * term (Eq. 7).  WF_ERR_CONFIG on an invalid shape, WF_ERR_ARG if
+ * bytes is null. */
+wf_status wf_workspace_bytes(int P, int C, int64_t N, int heads, int head_dim, int causal, size_t* bytes);
+
 /* Host-only: the plan of one rank: out[0..5] = {init_send, init_recv, next, last, R, regime}
  * (regime 0 = paper, 1 = extension). */
 wf_status wf_plan(int P, int C, int rank, int32_t out[6]);

@@ -250,6 +250,57 @@ uint32_t* flag_of(wf_ctx* ctx, int owner, int word) {
 }
 
 // ------------------------------------------------------------------ workspace
+// the workspace carve of one rank (bytes per buffer, in carve order)
+using CarveList = std::vector<std::pair<void**, int64_t>>;
+void carve_rank(const Geo& g, RankBufs& b, CarveList& items) {
+  const int64_t C = g.C, n = g.n, E = g.E, h = g.h, Bk = g.Bk;
+  const int64_t team = C * n * E;  // elements of a team tensor
+  auto add = [&](auto** p, int64_t bytes) { items.push_back({reinterpret_cast<void**>(p), bytes}); };
+  if (C > 1) {
+    add(&b.qt, team * 2);
+    add(&b.t_do, team * 2);
+    add(&b.t_lse, C * h * n * 4);
+    add(&b.t_dsum, C * h * n * 4);
+    add(&b.rs_o, team * 4);
+    add(&b.rs_lse, C * h * n * 4);
+    add(&b.rsq, team * 4);
+    if (g.paper) {
+      add(&b.kt, team * 2);
+      add(&b.vt, team * 2);
+    }
+  }
+  for (int s = 0; s < 2; ++s) {
+    add(&b.rk[s], Bk * E * 2);
+    add(&b.rv[s], Bk * E * 2);
+  }
+  add(&b.o_state, team * 4);
+  add(&b.lse_state, C * h * n * 4);
+  add(&b.dsum, h * n * 4);
+  for (int s = 0; s < 2; ++s) {
+    add(&b.pdq[s], team * 4);
+    if (g.R > 1) {
+      add(&b.pq[s], team * 2);
+      add(&b.pdo[s], team * 2);
+      add(&b.plse[s], C * h * n * 4);
+      add(&b.pdsum[s], C * h * n * 4);
+    }
+  }
+  if (g.R > 1) add(&b.home_dq, team * 4);
+  add(&b.dk_acc, Bk * E * 4);
+  add(&b.dv_acc, Bk * E * 4);
+  {  // dK/dV replica slots on the owner (holders of a unit: C paper, T extension)
+    const int64_t slots = g.paper ? C : g.T;
+    add(&b.rev_k, slots * n * E * 4);
+    add(&b.rev_v, slots * n * E * 4);
+  }
+}
+
+size_t carve_total(const CarveList& items) {
+  size_t total = kFlagBytes;
+  for (auto& it : items) total += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
+  return total;
+}
+
 wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   if (ctx->dry) {
     ctx->rb.assign(ctx->plan.P, RankBufs{});
@@ -266,53 +317,10 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
     ctx->ws = nullptr;
   }
   const int nranks = ctx->emulated ? g.P : 1;
-  const int64_t C = g.C, n = g.n, E = g.E, h = g.h, Bk = g.Bk;
-  const int64_t team = C * n * E;  // elements of a team tensor
-  // carve plan (bytes), per rank
-  std::vector<std::pair<void**, int64_t>> items;
+  CarveList items;
   std::vector<RankBufs> rb(nranks);
-  for (auto& b : rb) {
-    auto add = [&](auto** p, int64_t bytes) { items.push_back({reinterpret_cast<void**>(p), bytes}); };
-    if (C > 1) {
-      add(&b.qt, team * 2);
-      add(&b.t_do, team * 2);
-      add(&b.t_lse, C * h * n * 4);
-      add(&b.t_dsum, C * h * n * 4);
-      add(&b.rs_o, team * 4);
-      add(&b.rs_lse, C * h * n * 4);
-      add(&b.rsq, team * 4);
-      if (g.paper) {
-        add(&b.kt, team * 2);
-        add(&b.vt, team * 2);
-      }
-    }
-    for (int s = 0; s < 2; ++s) {
-      add(&b.rk[s], Bk * E * 2);
-      add(&b.rv[s], Bk * E * 2);
-    }
-    add(&b.o_state, team * 4);
-    add(&b.lse_state, C * h * n * 4);
-    add(&b.dsum, h * n * 4);
-    for (int s = 0; s < 2; ++s) {
-      add(&b.pdq[s], team * 4);
-      if (g.R > 1) {
-        add(&b.pq[s], team * 2);
-        add(&b.pdo[s], team * 2);
-        add(&b.plse[s], C * h * n * 4);
-        add(&b.pdsum[s], C * h * n * 4);
-      }
-    }
-    if (g.R > 1) add(&b.home_dq, team * 4);
-    add(&b.dk_acc, Bk * E * 4);
-    add(&b.dv_acc, Bk * E * 4);
-    {  // dK/dV replica slots on the owner (holders of a unit: C paper, T extension)
-      const int64_t slots = g.paper ? C : g.T;
-      add(&b.rev_k, slots * n * E * 4);
-      add(&b.rev_v, slots * n * E * 4);
-    }
-  }
-  size_t total = kFlagBytes;
-  for (auto& it : items) total += (static_cast<size_t>(it.second) + 1023) & ~size_t(1023);
+  for (auto& b : rb) carve_rank(g, b, items);
+  const size_t total = carve_total(items);
   void* base = nullptr;
   CK(cudaMalloc(&base, total));
   CK(cudaMemset(base, 0, kFlagBytes));
@@ -1348,6 +1356,23 @@ static wf_status copy_trace(const std::vector<wf_event>& a, const std::vector<wf
 wf_status wf_get_trace(wf_ctx* ctx, wf_event* buf, size_t cap, size_t* n_out) {
   if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
   return copy_trace(ctx->trace_fwd, ctx->trace_bwd, buf, cap, n_out);
+}
+
+wf_status wf_workspace_bytes(int P, int C, int64_t N, int heads, int head_dim, int causal, size_t* bytes) {
+  if (!bytes) return fail(nullptr, WF_ERR_ARG, "wf_workspace_bytes: null output");
+  wf_ctx* ctx = nullptr;
+  wf_ctx* tmp = nullptr;
+  WCK(new_ctx(P, C, &ctx, &tmp));
+  std::unique_ptr<wf_ctx> hold(ctx);
+  ctx->dry = true;
+  Geo g;
+  wf_status s = check_shape(ctx, N, heads, head_dim, causal, &g);
+  if (s != WF_OK) return fail(nullptr, s, ctx->err);
+  RankBufs b{};
+  CarveList items;
+  carve_rank(g, b, items);
+  *bytes = carve_total(items);
+  return WF_OK;
 }
 
 wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,

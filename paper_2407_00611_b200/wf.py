@@ -102,6 +102,13 @@ def shard_ranges(P, rank, N, causal):
     return list(out)
 
 
+def workspace_bytes(P, C, N, heads, head_dim, causal):
+    """Device workspace bytes one rank allocates for this shape (wf_workspace_bytes)."""
+    out = ctypes.c_size_t(0)
+    _check(lib().wf_workspace_bytes(P, C, N, heads, head_dim, int(causal), ctypes.byref(out)))
+    return int(out.value)
+
+
 class Context:
     """A wf_ctx: real (one rank of a torch.distributed job) or emulated (all P ranks on one GPU)."""
 
