@@ -24,13 +24,6 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-// for K tile at kpos0: 0 = q tile fully masked, 1 = full, 2 = diagonal
-__device__ __forceinline__ int qtile_kind(const BwdArgs& a, int kpos0, int it) {
-  if (!a.causal) return 1;
-  const int qp0 = tile_gpos(a.qpos, it);
-  return qp0 < kpos0 ? 0 : (qp0 == kpos0 ? 2 : 1);
-}
-
 template <int D>
 struct BwdCfg {
   static constexpr int DP = (D + 15) / 16 * 16;
@@ -103,8 +96,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int head = blockIdx.y;
   const int k0 = kt * WF_TILE;
   const int kpos0 = a.causal ? tile_gpos(a.kpos, kt) : k0;
-  const int nqt = a.nq / WF_TILE;
-  const bool tlon = a.tl && blockIdx.x == a.tl_cta && blockIdx.y == 0;
+  // query tiles that see this key tile: first position >= kpos0 (kind 2 when equal)
+  auto q_iter = [&]() { return VisIter<false>(a.qpos, a.causal != 0, kpos0); };
+  auto kind_at = [&](int qp) -> int { return (a.causal && qp == kpos0) ? 2 : 1; };
+  const bool tlon = a.tl && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.tl_cta;
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
@@ -152,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(smem + Cfg::OFF_V + p * Cfg::PANEL, &tmV, &bar[B_KV], p * 64, head, k0);
       }
       int ii = 0;
-      for (int it = 0; it < nqt; ++it) {
-        if (qtile_kind(a, kpos0, it) == 0) continue;
+      int it, qp;
+      for (auto iq = q_iter(); iq.next(a.qpos, it, qp);) {
         const int st = ii % QST;
         if (ii >= QST) mbar_wait(&bar[B_QE + st], ((ii - QST) / QST) & 1);
         tl_stamp(a.tl, tlon, 3, ii, 0);
@@ -166,8 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (lane == 1) {
       tma_prefetch_desc(&tmDO);
       int ii = 0;
-      for (int it = 0; it < nqt; ++it) {
-        if (qtile_kind(a, kpos0, it) == 0) continue;
+      int it, qp;
+      for (auto iq = q_iter(); iq.next(a.qpos, it, qp);) {
         const int ss = ii & 1;
         if (ii >= 2) mbar_wait(&bar[B_SE + ss], ((ii - 2) >> 1) & 1);
         mbar_arrive_expect_tx(&bar[B_SF + ss], 1024);
@@ -208,8 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bar[B_S]);
       };
-      int ntiles = 0;
-      for (int it = 0; it < nqt; ++it) ntiles += qtile_kind(a, kpos0, it) != 0;
+      const int ntiles = q_iter().count(a.qpos);
       mbar_wait(&bar[B_KV], 0);
       tc_fence_after();
       if (ntiles > 0) issue_s(0);
@@ -267,9 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tl = tbase + (static_cast<uint32_t>(wq * 32) << 16);
     uint8_t* sds = smem + Cfg::OFF_DS + hf * Cfg::PANEL + (r >> 3) * 1024 + (r & 7) * 128;
     int ii = 0;
-    for (int it = 0; it < nqt; ++it) {
-      const int kind = qtile_kind(a, kpos0, it);
-      if (kind == 0) continue;
+    int it, qp;
+    for (auto iq = q_iter(); iq.next(a.qpos, it, qp);) {
+      const int kind = kind_at(qp);
       const int ss = ii & 1;
       const float* slse = stat + ss * 256 + hf * 64;
       const float* sdd = stat + ss * 256 + 128 + hf * 64;
@@ -420,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tl = tbase + (static_cast<uint32_t>(warp * 32) << 16);
     uint8_t* wbox0 = smem + Cfg::OFF_STG + warp * 8192;
     int ii = 0, chunk = 0;
-    for (int it = 0; it < nqt; ++it) {
-      if (qtile_kind(a, kpos0, it) == 0) continue;
+    int it, qp;
+    for (auto iq = q_iter(); iq.next(a.qpos, it, qp);) {
       mbar_wait(&bar[B_DQF], ii & 1);
       tc_fence_after();
       tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 0);

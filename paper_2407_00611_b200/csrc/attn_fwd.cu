@@ -17,6 +17,8 @@
 #include "common.h"
 #include "sm100.cuh"
 
+#include <type_traits>
+
 namespace wf {
 using namespace sm100;
 
@@ -27,13 +29,6 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU)
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
-
-// 0 = fully masked (skip), 1 = fully visible, 2 = diagonal
-__device__ __forceinline__ int tile_kind(const FwdArgs& a, int qpos0, int jt) {
-  if (!a.causal) return 1;
-  int kp0 = tile_gpos(a.kpos, jt);
-  return kp0 > qpos0 ? 0 : (kp0 == qpos0 ? 2 : 1);
-}
 
 template <int D>
 struct FwdCfg {
@@ -83,15 +78,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int ntile = hasB ? 2 : 1;
   const int qposA = a.causal ? tile_gpos(a.qpos, q0 / WF_TILE) : q0;
   const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, q0 / WF_TILE + 1) : q0 + WF_TILE;
-  const int nkt = a.nk / WF_TILE;
   const bool has_state = a.o_in != nullptr;
-  const bool tlon = a.tl && blockIdx.x == a.tl_cta && blockIdx.y == 0;
-  // kind of (query tile t, key tile jt): 0 masked, 1 full, 2 diagonal
-  auto kind_of = [&](int t, int jt) -> int {
+  const bool tlon = a.tl && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.tl_cta;
+  // kind of (query tile t, key tile starting at global position kp): 0 masked, 1 full, 2 diagonal
+  auto kind_of = [&](int t, int kp) -> int {
     if (t == 1 && !hasB) return 0;
-    return tile_kind(a, t == 0 ? qposA : qposB, jt);
+    if (!a.causal) return 1;
+    const int qp = t == 0 ? qposA : qposB;
+    return kp > qp ? 0 : (kp == qp ? 2 : 1);
   };
-  auto visible = [&](int jt) -> bool { return kind_of(0, jt) != 0 || kind_of(1, jt) != 0; };
+  // key tiles visible to either query tile: first position <= the larger query tile start
+  const int qbound = hasB ? max(qposA, qposB) : qposA;
+  auto kv_iter = [&]() { return VisIter<true>(a.kpos, a.causal != 0, qbound); };
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment
@@ -131,22 +129,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int p = 0; p < Cfg::NP; ++p)
           tma_load_3d(smem + Cfg::OFF_Q + t * Cfg::TILE + p * Cfg::PANEL, &tmQ, &bar[B_Q], p * 64, head,
                       q0 + t * WF_TILE);
-      int jj = 0;
-      for (int jt = 0; jt < nkt; ++jt) {
-        if (!visible(jt)) continue;
+      int jj = 0, jt, kp;
+      for (auto it = kv_iter(); it.next(a.kpos, jt, kp);) {
         const int st = jj % kKStages;
         if (jj >= kKStages) mbar_wait(&bar[B_KE + st], ((jj - kKStages) / kKStages) & 1);
         tl_stamp(a.tl, tlon, 3, jj, 0);
         uint8_t* sk = smem + Cfg::OFF_K + st * Cfg::TILE;
         mbar_arrive_expect_tx(&bar[B_K + st], Cfg::TILE);
         for (int p = 0; p < Cfg::NP; ++p) tma_load_3d(sk + p * Cfg::PANEL, &tmK, &bar[B_K + st], p * 64, head, jt * WF_TILE);
+        if (tlon && jj == 0) {  // debug timeline: arrival of Q and of the first K tile
+          mbar_wait(&bar[B_Q], 0);
+          tl_stamp(a.tl, tlon, 3, 0, 1);
+          mbar_wait(&bar[B_K], 0);
+          tl_stamp(a.tl, tlon, 3, 0, 2);
+        }
         ++jj;
       }
     } else if (lane == 1) {
       tma_prefetch_desc(&tmV);
-      int jj = 0;
-      for (int jt = 0; jt < nkt; ++jt) {
-        if (!visible(jt)) continue;
+      int jj = 0, jt, kp;
+      for (auto it = kv_iter(); it.next(a.kpos, jt, kp);) {
         const int st = jj & 1;
         if (jj >= 2) mbar_wait(&bar[B_VE + st], ((jj - 2) >> 1) & 1);
         uint8_t* sv = smem + Cfg::OFF_V + st * Cfg::TILE;
@@ -183,8 +185,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mma_ts(tbase + 256 + t * 128, tbase + t * 128 + k * 8, smem_desc_sw128(sV + k * 2048, Cfg::PANEL, 1024),
                  idO, (j > 0 || has_state || k > 0) ? 1u : 0u);
       };
-      int nvis = 0;
-      for (int jt = 0; jt < nkt; ++jt) nvis += visible(jt);
+      const int nvis = kv_iter().count(a.kpos);
       mbar_wait(&bar[B_Q], 0);
       for (int j = 0; j < nvis; ++j) {
         tl_stamp(a.tl, tlon, 0, j, 0);
@@ -241,9 +242,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_wait_st();
       }
       int j = 0;
-      for (int jt = 0; jt < nkt; ++jt) {
-        if (!visible(jt)) continue;
-        const int kind = kind_of(t, jt);
+      // one key tile; DIAG selects the masked variant (diagonal or fully masked tile) so the
+      // common, fully visible path carries no per-element select and no register shuffle
+      auto tile = [&](auto diag_c, const int kind) {
+        constexpr bool DIAG = decltype(diag_c)::value;
         mbar_wait(&bar[B_S + t], j & 1);
         tc_fence_after();
         tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 0);
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tmem_ld32(tl + cS + 64, r2);
           tmem_ld32(tl + cS + 96, r3);
           tmem_wait_ld();
+          tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 2);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             s[i] = __uint_as_float(r0[i]);
@@ -263,10 +266,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             s[96 + i] = __uint_as_float(r3[i]);
           }
         }
-        if (kind != 1) {
+        if constexpr (DIAG) {
+          const int lim = kind == 0 ? -1 : row;  // keys c <= lim are visible
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (kind == 0 || c > row) s[c] = -INFINITY;
+          for (int c = 0; c < 128; ++c) s[c] = c > lim ? -INFINITY : s[c];
         }
         // row max as 8 independent chains (3-input FMNMX), then a small tree: a single
         // 128-long dependent chain would cost ~500 cycles of latency per tile
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           l *= alpha;
           m = mnew;
         }
+        tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 3);
         const float mm = (m == -INFINITY) ? 0.f : m;
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mm, -mm);
         float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -327,6 +331,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 1);
         l += rs;
         ++j;
+      };
+      int jt, kp;
+      for (auto it = kv_iter(); it.next(a.kpos, jt, kp);) {
+        const int kind = kind_of(t, kp);
+        if (kind == 1)
+          tile(std::integral_constant<bool, false>{}, kind);
+        else
+          tile(std::integral_constant<bool, true>{}, kind);
       }
       // epilogue
       mbar_wait(&bar[B_OF + t], 0);

@@ -128,6 +128,9 @@ extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, i
   if (causal) {
     if (!fill_postable(&a.qpos, nq, chunk, qstart, nqchunks) || !fill_postable(&a.kpos, nk, chunk, kstart, nkchunks))
       return set_err(WF_ERR_CONFIG, "wf_block_fwd: bad chunk table");
+  } else {  // positions are irrelevant without a mask; contiguous tables drive the tile loops
+    fill_postable(&a.qpos, nq, 0, nullptr, 0);
+    fill_postable(&a.kpos, nk, 0, nullptr, 0);
   }
   a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(head_dim));
   a.o_in = o_in;
@@ -161,6 +164,9 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
   if (causal) {
     if (!fill_postable(&a.qpos, nq, chunk, qstart, nqchunks) || !fill_postable(&a.kpos, nk, chunk, kstart, nkchunks))
       return set_err(WF_ERR_CONFIG, "wf_block_bwd: bad chunk table");
+  } else {  // positions are irrelevant without a mask; contiguous tables drive the tile loops
+    fill_postable(&a.qpos, nq, 0, nullptr, 0);
+    fill_postable(&a.kpos, nk, 0, nullptr, 0);
   }
   a.scale = 1.f / std::sqrt(static_cast<float>(head_dim));
   a.scale_log2 = 1.4426950408889634f * a.scale;

@@ -38,6 +38,54 @@ __host__ __device__ __forceinline__ int tile_gpos(const PosTable& t, int tile) {
   const int row0 = tile * 128;
   return t.start[row0 / t.chunk] + row0 % t.chunk;
 }
+// Visible 128-row tiles of a block, chunk by chunk.  Positions increase inside a chunk, so
+// under the causal rule the visible tiles of a chunk are a prefix (KEYS: first position
+// <= bound, the query side's last tile start) or a suffix (QUERIES: first position >=
+// bound, the key tile's start); one table read per chunk instead of a position lookup per
+// tile (the per-tile lookups went through local memory and cost ~40k cycles per CTA).
+template <bool KEYS>
+struct VisIter {
+  int c, i, hi, s, tpc, bound;
+  bool causal;
+  __device__ __forceinline__ VisIter(const PosTable& t, bool causal_, int bound_)
+      : c(-1), i(0), hi(0), s(0), tpc(t.chunk >> 7), bound(bound_), causal(causal_) {}
+  __device__ __forceinline__ void range(int st, int& lo, int& h) const {
+    if (!causal) {
+      lo = 0;
+      h = tpc;
+    } else if (KEYS) {
+      const int d = bound - st;
+      lo = 0;
+      h = d < 0 ? 0 : ((d >> 7) + 1 < tpc ? (d >> 7) + 1 : tpc);
+    } else {
+      const int d = bound - st;
+      lo = d <= 0 ? 0 : (((d + 127) >> 7) < tpc ? ((d + 127) >> 7) : tpc);
+      h = tpc;
+    }
+  }
+  // next visible tile: its index in the block and its first global position
+  __device__ __forceinline__ bool next(const PosTable& t, int& tile, int& pos) {
+    while (i >= hi) {
+      if (++c >= t.nchunks) return false;
+      s = t.start[c];
+      range(s, i, hi);
+    }
+    tile = c * tpc + i;
+    pos = s + (i << 7);
+    ++i;
+    return true;
+  }
+  __device__ __forceinline__ int count(const PosTable& t) const {
+    int n = 0;
+    for (int cc = 0; cc < t.nchunks; ++cc) {
+      int lo, h;
+      range(t.start[cc], lo, h);
+      n += h - lo;
+    }
+    return n;
+  }
+};
+
 inline int tpc_shift_of(int chunk) {
   const int tpc = chunk / 128;
   int sh = 0;

@@ -865,7 +865,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
 wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, const bf16* K, const bf16* V,
                    const bf16* O, const float* LSE, bf16* dQ, bf16* dK, bf16* dV, cudaStream_t st) {
   const Plan& pl = ctx->plan;
-  const int P = g.P, C = g.C, R = g.R, T = g.T;
+  const int P = g.P, C = g.C, R = g.R;
   const int64_t n = g.n, E = g.E, h = g.h, team = static_cast<int64_t>(C) * n * E;
   auto off = [&](int r, int64_t per) { return ctx->emulated ? r * per : 0; };
   auto L = [&](int r, auto* p, int64_t per) { return local(ctx, r) ? p + off(r, per) : decltype(p)(nullptr); };

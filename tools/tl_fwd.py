@@ -7,6 +7,6 @@ print('kv tiles',n,'period', np.diff(t[0,10:n,0]).mean())
 print('MMA: start->PV0 issued',med(t[0,:n,1]-t[0,:n,0]),'->S0 issued',med(t[0,:n,2]-t[0,:n,1]),'->PV1 issued',med(t[0,:n,3]-t[0,:n,2]),'->S1 issued',med(t[0,:n,4]-t[0,:n,3]),'-> next start',med(np.r_[t[0,1:n,0]-t[0,:n-1,4],0]))
 for r in (1,2):
     sm=t[r,:n,1]-t[r,:n,0]; w=np.r_[t[r,1:n,0]-t[r,:n-1,1],0]
-    print('softmax WG',r-1,'phase',med(sm),'wait next S',med(w))
-#print('TMA K issue -> S0 issue', med(t[0,:n,2]-t[3,:n,0]))
-for j in range(100,103): print(j, t[0,j,:5], t[1,j,:2], t[2,j,:2], t[3,j,0])
+    print('softmax WG',r-1,'phase',med(sm),'(ld',med(t[r,:n,2]-t[r,:n,0]),'max',med(t[r,:n,3]-t[r,:n,2]),'exp',med(t[r,:n,1]-t[r,:n,3]),') wait next S',med(w))
+    # S_t(j) issued (MMA stamp) -> softmax sees S
+    print('   S issue -> seen', med(t[r,:n,0]-t[0,:n,2*r]), ' P arrive -> PV issued(next j)', med(t[0,1:n+1,2*r-1][:n]-t[r,:n,1]) if n+1<=t.shape[1] else '')
