@@ -94,6 +94,20 @@ wf_status wf_init_emulated(int P, int C, wf_ctx** out);
 wf_status wf_attn_fwd(wf_ctx* ctx, const void* Q, const void* K, const void* V, int64_t N, int heads,
                       int head_dim, int causal, void* O, float* LSE, void* stream);
 
+/* QKV projection fused with the team all-gather (Alg. 1 l.1
+ * "AllGather_QKVmatmul").  X bf16 [N/P, hidden]
+ * (this rank's shard of the layer input), W bf16 [3 heads head_dim, hidden] (row-major,
+ * the stacked W_q; W_k; W_v of nn.Linear, replicated on every rank) ->
+ * Q, K, V bf16 [N/P, heads, head_dim] = X W^T split in three.  With C > 1 the GEMM's
+ * epilogue also stores every output tile into the team members' gathered buffers (peer
+ * memory; in the extension regime K/V go to the ranks whose slice holds this unit), so
+ * the next wf_attn_fwd on this context with these Q, K, V skips the gather copies (its
+ * CommTrace is unchanged: the same messages, moved by the epilogue).  Emulated mode:
+ * X [P][N/P, hidden], outputs [P][N/P, heads, head_dim].  hidden: multiple of 64;
+ * N/P: multiple of 128; heads * head_dim: multiple of 128.  WF_ERR_CONFIG otherwise. */
+wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int hidden, int heads, int head_dim,
+                      int causal, void* Q, void* K, void* V, void* stream);
+
 /* Backward: given dO and the forward's Q, K, V, O, LSE (same
  * shapes as wf_attn_fwd) -> dQ, dK, dV bf16 [N/P, heads, head_dim]. */
 wf_status wf_attn_bwd(wf_ctx* ctx, const void* dO, const void* Q, const void* K, const void* V, const void* O,
@@ -167,6 +181,11 @@ wf_status wf_block_fwd(const void* q, const void* k, const void* v, int nq, int 
                        int causal, int chunk, const int32_t* qstart, int nqchunks, const int32_t* kstart,
                        int nkchunks, const float* o_in, const float* lse_in, float* o_out, void* o_bf16,
                        float* lse_out, void* stream);
+
+/* wf_gemm_bf16: Y = A B^T on the tensor cores (the projection GEMM of wf_qkv_proj),
+ * A bf16 [M, K], B bf16 [N, K], Y bf16 [M, N], all row-major, fp32 accumulation.
+ * M multiple of 128, N of 128, K of 64 (WF_ERR_CONFIG otherwise); 16-byte aligned. */
+wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* Y, void* stream);
 
 /* wf_block_bwd: PAPER.md:203 one flash-attention backward step: the K/V block
  * (stationary) against query rows q with dO, final LSE and D = rowsum(dO o O) [heads, nq].

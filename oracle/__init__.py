@@ -14,6 +14,7 @@ blocks    -- the per-block primitives the paper's loop is built from:
              flash-attention backward step (§3.2.1 "Backward Propagation").
 topology  -- Alg. 2 get_init_send, its inverse, Alg. 3 get_P2P_config.
 sharding  -- §3.5 naive / zigzag dataloader.
+proj      -- the QKV projection of Alg. 1 l.1 (AllGather_QKVmatmul).
 schedule  -- literal simulation of Alg. 1 + the two-loop backward, rank by
              rank, with fp64 payloads and a CommTrace.
 

@@ -55,6 +55,19 @@ bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int he
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 static unsigned long long* g_tl = nullptr;
 static int g_tl_cta = 0;
 unsigned long long* timeline_buffer() { return g_tl; }
@@ -182,6 +195,29 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
       !make_tmap_rows(&tv, v, nk, heads, head_dim) || !make_tmap_rows(&tdo, dO, nq > 0 ? nq : WF_TILE, heads, head_dim))
     return set_err(WF_ERR_ARG, "wf_block_bwd: TMA map encode failed (alignment?)");
   cudaError_t e = launch_block_bwd(tq, tk, tv, tdo, a, head_dim, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
+  return WF_OK;
+}
+
+extern "C" wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* Y, void* stream) {
+  if (!A || !B || !Y) return set_err(WF_ERR_ARG, "wf_gemm_bf16: null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Y)) & 15)
+    return set_err(WF_ERR_ARG, "wf_gemm_bf16: pointers must be 16-byte aligned");
+  if (M <= 0 || M % 128 || N <= 0 || N % 128 || K <= 0 || K % 64)
+    return set_err(WF_ERR_CONFIG, "wf_gemm_bf16: M, N multiples of 128 and K of 64 required");
+  const int bn = N % 256 == 0 ? 256 : 128;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d(&ta, A, M, K, 128) || !make_tmap_2d(&tb, B, N, K, bn))
+    return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.split = N;
+  g.ndst[0] = 1;
+  g.ld = N;
+  g.out[0][0] = static_cast<__nv_bfloat16*>(Y);
+  cudaError_t e = launch_gemm(ta, tb, g, bn, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
   return WF_OK;
 }

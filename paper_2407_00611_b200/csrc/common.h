@@ -141,6 +141,24 @@ int timeline_cta();
 // Host: 3-D TMA map over a [rows, heads, D] fp32 tensor, box {32, 1, 32}, SW128 (dQ reduce-add).
 bool make_tmap_f32_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
 
+// Host: 2-D TMA map over a row-major [rows, cols] bf16 matrix, box {64, box_rows}, SW128.
+bool make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+
+// Y = A B^T (bf16 in, fp32 accumulate, bf16 out), A [M, K], B [N, K] row-major (the QKV
+// projection of PAPER.md Alg. 1 l.1).  Output column c belongs to part c / split (Q, K, V)
+// at column c % split of a row-major [M, split] matrix with leading dimension ld; every
+// tile is stored to ndst destinations of its part (the caller's tensor and, fused, the
+// team members' gathered buffers over peer memory).
+#define WF_GEMM_MAX_DST 6
+struct GemmArgs {
+  int M, N, K;
+  int split;
+  int ndst[3];                    // destinations per part
+  int64_t ld;
+  __nv_bfloat16* out[3][WF_GEMM_MAX_DST];
+};
+cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, cudaStream_t s);
+
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
 cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

@@ -68,7 +68,8 @@ struct Seg {
 struct Xfer {
   int pass, kind, step, src, dst, block;
   std::vector<Seg> segs;
-  bool pull = false;  // peer-memory transport: the consumer kernel reads the source in place
+  bool pull = false;   // peer-memory transport: the consumer kernel reads the source in place
+  bool fused = false;  // already delivered by a producer kernel's epilogue (wf_qkv_proj)
 };
 
 constexpr size_t kFlagBytes = 4096;  // flag block at the start of every rank's workspace
@@ -96,6 +97,9 @@ struct wf_ctx {
   int64_t launches = 0;
   std::string err;
   int debug = 0;
+  // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V)
+  const void *proj_q = nullptr, *proj_k = nullptr, *proj_v = nullptr;
+  int64_t proj_key[4] = {0, 0, 0, 0};
   // peer-memory transport (real mode, P > 1): CUDA IPC mapped workspaces + flag signalling
   bool ipc = false;
   std::vector<char*> peer_base;
@@ -360,7 +364,8 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
   if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
   if (ctx->emulated) {
     for (const Xfer& x : xs)
-      for (const Seg& s : x.segs)
+      if (!x.fused)
+        for (const Seg& s : x.segs)
         if (s.bytes && s.src != s.dst) CK(cudaMemcpyAsync(s.dst, s.src, s.bytes, cudaMemcpyDeviceToDevice, st));
     return WF_OK;
   }
@@ -369,7 +374,7 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
     const int ch = st == ctx->comm_stream ? 1 : 0;
     cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
     for (const Xfer& x : xs) {
-      if (x.src != me || x.pull) continue;
+      if (x.src != me || x.pull || x.fused) continue;
       for (const Seg& sg : x.segs)
         if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
     }
@@ -443,7 +448,7 @@ wf_status run_phase_per_source(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<w
   const int ch = st == ctx->comm_stream ? 1 : 0;
   cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
   for (const Xfer& x : xs) {
-    if (x.src != me || x.pull) continue;
+    if (x.src != me || x.pull || x.fused) continue;
     for (const Seg& sg : x.segs)
       if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
   }
@@ -591,6 +596,11 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_fwd;
   tr.clear();
+  // gathers already delivered by wf_qkv_proj's epilogue (same tensors, same geometry)
+  const int64_t key[4] = {g.N, g.h, g.d, g.causal};
+  const bool pre = ctx->proj_q && ctx->proj_q == Q && ctx->proj_k == K && ctx->proj_v == V &&
+                   std::equal(key, key + 4, ctx->proj_key);
+  ctx->proj_q = ctx->proj_k = ctx->proj_v = nullptr;
   WCK(ipc_barrier(ctx, st));
 
   // Team tensors (C = 1: the caller's shard itself).
@@ -615,6 +625,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (p == r) continue;  // my own rows are read from the caller's buffer
         Xfer x{0, WF_KIND_AG_Q, -1, r, p, r, {}};
         x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+        x.fused = pre;
         xs.push_back(x);
       }
       const int ar = r % C;
@@ -622,6 +633,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (u == r) continue;
         const int64_t off = static_cast<int64_t>(u - ar * g.W) * n * E;
         Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+        x.fused = pre;
         x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
         x.segs.push_back({Vin(u), at(lp(r, B(ctx, r).rv[0]), off), n * E * 2});
         xs.push_back(x);
@@ -676,9 +688,11 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         for (int p = t * C; p < t * C + C; ++p) {
           Xfer x{0, WF_KIND_AG_Q, -1, r, p, r, {}};
           x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
+          x.fused = pre;
           xs.push_back(x);
           if (g.paper) {
             Xfer y{0, WF_KIND_AG_KV, -1, r, p, r, {}};
+            y.fused = pre;
             y.segs.push_back({Kin(r), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
             y.segs.push_back({Vin(r), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
             xs.push_back(y);
@@ -719,6 +733,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
           const int64_t off = static_cast<int64_t>(u - a * g.W) * n * E;
           Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
+          x.fused = pre;
           x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
           x.segs.push_back({Vin(u), at(lp(r, B(ctx, r).rv[0]), off), n * E * 2});
           xs.push_back(x);
@@ -1321,6 +1336,84 @@ wf_status wf_attn_fwd(wf_ctx* ctx, const void* Q, const void* K, const void* V, 
   WCK(ensure_ws(ctx, g));
   return forward(ctx, g, static_cast<const bf16*>(Q), static_cast<const bf16*>(K), static_cast<const bf16*>(V),
                  static_cast<bf16*>(O), LSE, static_cast<cudaStream_t>(stream));
+}
+
+wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int hidden, int heads, int head_dim,
+                      int causal, void* Q, void* K, void* V, void* stream) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  if (!X || !W || !Q || !K || !V) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: null pointer");
+  for (const void* p : {X, W, static_cast<const void*>(Q), static_cast<const void*>(K), static_cast<const void*>(V)})
+    if (!aligned16(p)) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: pointers must be 16-byte aligned");
+  Geo g;
+  WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
+  const int64_t n = g.n, E = g.E;
+  if (hidden <= 0 || hidden % 64 || E % 128 || n % 128)
+    return fail(ctx, WF_ERR_CONFIG, "wf_qkv_proj: hidden % 64, (heads*head_dim) % 128 and (N/P) % 128 must be 0");
+  WCK(ensure_ws(ctx, g));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int P = g.P, C = g.C;
+  const int bn = E % 256 == 0 ? 256 : 128;
+  CUtensorMap tw;
+  if (!make_tmap_2d(&tw, W, 3 * E, hidden, bn)) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
+  // fused gather: the epilogue writes straight into the team buffers (peer memory or, emulated,
+  // the virtual ranks' workspaces); the NCCL transport keeps the separate gather.
+  bool fuse = C > 1 && (ctx->emulated || ctx->ipc) && !(ctx->debug & WF_DEBUG_NO_TRANSFER);
+  if (fuse && !g.paper && C + 1 > WF_GEMM_MAX_DST) fuse = false;
+  if (fuse && ctx->ipc) WCK(ipc_barrier(ctx, st));  // every peer is done with its team buffers
+  auto lp = [&](int r, bf16* p) { return addressable(ctx, r) ? p : nullptr; };
+  for (int r = 0; r < P; ++r) {
+    if (!local(ctx, r)) continue;
+    const int64_t ro = ctx->emulated ? r : 0;
+    GemmArgs ga{};
+    ga.M = static_cast<int>(n);
+    ga.N = static_cast<int>(3 * E);
+    ga.K = hidden;
+    ga.split = static_cast<int>(E);
+    ga.ld = E;
+    bf16* outs[3] = {static_cast<bf16*>(Q) + ro * n * E, static_cast<bf16*>(K) + ro * n * E,
+                     static_cast<bf16*>(V) + ro * n * E};
+    for (int part = 0; part < 3; ++part) {
+      ga.out[part][0] = outs[part];
+      ga.ndst[part] = 1;
+    }
+    if (fuse) {
+      const int t = r / C, j = r - t * C;
+      auto add = [&](int part, bf16* p) -> bool {
+        if (!p || ga.ndst[part] >= WF_GEMM_MAX_DST) return false;
+        ga.out[part][ga.ndst[part]++] = p;
+        return true;
+      };
+      bool ok = true;
+      for (int p = t * C; p < t * C + C; ++p) {  // Alg. 1 l.1: member-major team tensors
+        ok = ok && add(0, at(lp(p, B(ctx, p).qt), j * n * E));
+        if (g.paper) {
+          ok = ok && add(1, at(lp(p, B(ctx, p).kt), j * n * E));
+          ok = ok && add(2, at(lp(p, B(ctx, p).vt), j * n * E));
+        }
+      }
+      if (!g.paper) {  // extension: unit r goes to the ranks whose K/V slice holds it
+        const int a = r / g.W;
+        const int64_t off = static_cast<int64_t>(r - a * g.W) * n * E;
+        for (int p = a; p < P; p += C) {
+          ok = ok && add(1, at(lp(p, B(ctx, p).rk[0]), off));
+          ok = ok && add(2, at(lp(p, B(ctx, p).rv[0]), off));
+        }
+      }
+      if (!ok) return fail(ctx, WF_ERR_CONFIG, "wf_qkv_proj: too many gather destinations");
+    }
+    CUtensorMap tx;
+    if (!make_tmap_2d(&tx, static_cast<const bf16*>(X) + ro * n * hidden, n, hidden, 128))
+      return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
+    WCK(kcheck(ctx, launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
+  }
+  if (fuse) {
+    ctx->proj_q = Q;
+    ctx->proj_k = K;
+    ctx->proj_v = V;
+    const int64_t key[4] = {g.N, g.h, g.d, g.causal};
+    std::copy(key, key + 4, ctx->proj_key);
+  }
+  return WF_OK;
 }
 
 wf_status wf_attn_bwd(wf_ctx* ctx, const void* dO, const void* Q, const void* K, const void* V, const void* O,

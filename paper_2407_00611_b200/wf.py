@@ -66,6 +66,15 @@ def block_fwd(q, k, v, causal=False, chunk=0, qstart=None, kstart=None, o_in=Non
     return of, ob, lse
 
 
+def gemm_bf16(a, b, y=None):
+    """Y = A B^T on the tensor cores (wf_gemm_bf16): a [M, K], b [N, K] bf16 -> y [M, N] bf16."""
+    M, K = a.shape
+    N = b.shape[0]
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=a.device) if y is None else y
+    _check(lib().wf_gemm_bf16(_ptr(_bf16(a, "a")), _ptr(_bf16(b, "b")), M, N, K, _ptr(_bf16(y, "y")), _stream()))
+    return y
+
+
 def block_bwd(q, k, v, do, lse, dsum, dq_acc, dk_acc, dv_acc, causal=False, chunk=0, qstart=None, kstart=None,
               accumulate=False):
     """One flash-attention backward step on the current device (in place on the accumulators)."""
@@ -140,6 +149,17 @@ class Context:
         _check(lib().wf_attn_fwd(self.h, _ptr(q), _ptr(k), _ptr(v), N, h, d, int(causal), _ptr(o), _ptr(lse),
                                  _stream()), self.h)
         return o, lse
+
+    def qkv_proj(self, x, w, N, heads, head_dim, causal, q=None, k=None, v=None):
+        """Alg. 1 l.1 AllGather_QKVmatmul (wf_qkv_proj): x [rows, hidden], w [3 heads head_dim, hidden]
+        -> q, k, v [rows, heads, head_dim]; with C > 1 the team gather rides on the GEMM epilogue."""
+        rows, hidden = x.shape
+        q = torch.empty((rows, heads, head_dim), dtype=torch.bfloat16, device=x.device) if q is None else q
+        k = torch.empty_like(q) if k is None else k
+        v = torch.empty_like(q) if v is None else v
+        _check(lib().wf_qkv_proj(self.h, _ptr(_bf16(x, "x")), _ptr(_bf16(w, "w")), N, hidden, heads, head_dim,
+                                 int(causal), _ptr(q), _ptr(k), _ptr(v), _stream()), self.h)
+        return q, k, v
 
     def bwd(self, do, q, k, v, o, lse, N, causal, dq=None, dk=None, dv=None):
         rows, h, d = q.shape

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import torch
 
-__all__ = ["make_qkv_do", "to_f64"]
+__all__ = ["make_qkv_do", "make_x_w", "to_f64"]
 
 
 def make_qkv_do(N: int, heads: int, head_dim: int, seed: int = 0, peaky: bool = False):
@@ -28,6 +28,15 @@ def make_qkv_do(N: int, heads: int, head_dim: int, seed: int = 0, peaky: bool = 
     if peaky:
         q = q * 4.0
     return tuple(t.to(torch.bfloat16).contiguous() for t in (q, k, v, do))
+
+
+def make_x_w(rows: int, hidden: int, heads: int, head_dim: int, seed: int = 0):
+    """Return (X, W) CPU bf16 for the QKV projection (Alg. 1 l.1): X [rows, hidden] ~ N(0, 1),
+    W [3 heads head_dim, hidden] ~ N(0, 1/hidden) (nn.Linear-style scale, so Q/K/V ~ N(0, 1))."""
+    g = torch.Generator().manual_seed(int(seed) + 1000)
+    x = torch.randn((rows, hidden), generator=g, dtype=torch.float32)
+    w = torch.randn((3 * heads * head_dim, hidden), generator=g, dtype=torch.float32) * hidden ** -0.5
+    return x.to(torch.bfloat16).contiguous(), w.to(torch.bfloat16).contiguous()
 
 
 def to_f64(t):
