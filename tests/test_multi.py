@@ -144,3 +144,56 @@ def test_nccl_real_path(C, causal):
         assert all(e[3] == r for e in tr)
         trace += tr
     assert Counter(trace) == Counter(_oracle_events(world, C, N, h, d, causal))
+
+
+def _proj_worker(rank, world, port, C, N, causal, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import paper_2407_00611_b200 as wf
+        from wf_inputs import make_x_w
+        from oracle.sharding import unit_positions
+        h, d, H = 2, 128, 192
+        xg, w = make_x_w(N, H, h, d, seed=4)
+        idx = torch.from_numpy(unit_positions(rank, world, N, causal))
+        xs = xg[idx].contiguous().cuda()
+        ctx = wf.Context(world, C, rank=rank)
+        qs, ks, vs = ctx.qkv_proj(xs, w.cuda(), N, h, d, causal)
+        o1, l1 = ctx.fwd(qs, ks, vs, N, causal)
+        torch.cuda.synchronize()
+        tr1 = ctx.trace()
+        ctx.close()
+        ctx = wf.Context(world, C, rank=rank)
+        o2, l2 = ctx.fwd(qs.clone(), ks.clone(), vs.clone(), N, causal)
+        torch.cuda.synchronize()
+        tr2 = ctx.trace()
+        ctx.close()
+        same = bool(torch.equal(o1, o2) and torch.equal(l1, l2))
+        allres = [None] * world
+        dist.all_gather_object(allres, (same, sorted(tr1) == sorted(tr2)))
+        if rank == 0:
+            q.put(allres)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.parametrize("C", [2, 4])
+def test_fused_projection_gather_real_path(C):
+    world = min(torch.cuda.device_count(), 4)
+    if world % C:
+        pytest.skip("C must divide the GPU count")
+    N = 512 * world
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proj_worker, args=(r, world, port, C, N, True, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allres = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(same and tr for same, tr in allres), allres
