@@ -48,6 +48,9 @@ enum {
   B_DS = 16, B_DQF = 17, B_DQE = 18, B_DSE = 19, B_DONE = 20, B_NUM = 21
 };
 
+#ifndef WF_BWD_POLY_EVERY
+#define WF_BWD_POLY_EVERY 0  // every k-th exponential pair of the P phase on the FMA pipe
+#endif
 #ifndef WF_DQ_ATOMIC
 #define WF_DQ_ATOMIC 0
 #endif
@@ -305,7 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int q = c * 32 + 2 * i;
             const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])), sc2,
                                    *reinterpret_cast<const float2*>(slse + q));
+#if WF_BWD_POLY_EVERY > 0
+            if ((c * 16 + i) % WF_BWD_POLY_EVERY == WF_BWD_POLY_EVERY - 1) {
+              const float2 e = poly_exp2x2(x);
+              pk[c * 16 + i] = pack_bf16x2(e.x, e.y);
+            } else {
+              pk[c * 16 + i] = pack_bf16x2(fast_exp2(x.x), fast_exp2(x.y));
+            }
+#else
             pk[c * 16 + i] = pack_bf16x2(fast_exp2(x.x), fast_exp2(x.y));
+#endif
           }
         }
       }

@@ -97,6 +97,7 @@ struct wf_ctx {
   int64_t launches = 0;
   std::string err;
   int debug = 0;
+  bool emu_unitpipe = false;  // emulated: run the extension regime unit-pipelined (WF_EMU_UNITPIPE=1)
   // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V)
   const void *proj_q = nullptr, *proj_k = nullptr, *proj_v = nullptr;
   int64_t proj_key[4] = {0, 0, 0, 0};
@@ -612,9 +613,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   // the K/V slice pull run on the comm stream with one completion event per source rank;
   // the step is cut into (query unit, key unit) launches that merge into the same (O, lse)
   // state, the locally present units first, so the transfers overlap the compute.
-  const bool unitpipe = ctx->ipc && !g.paper && C > 1;
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && !g.paper && C > 1;
   if (unitpipe) {
-    const int me = ctx->rank, t = me / C, a = me % C;
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
@@ -639,7 +639,13 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         xs.push_back(x);
       }
     }
-    WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    if (ctx->ipc)
+      WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    else
+      WCK(run_phase(ctx, xs, tr, st));  // emulated: device copies in stream order
+    for (int me = 0; me < P; ++me) {
+    if (!local(ctx, me)) continue;
+    const int t = me / C, a = me % C;
     RankBufs& b = B(ctx, me);
     std::vector<int> qorder, korder;
     for (int i = 0; i < C; ++i) qorder.push_back(t * C + (a + i) % C);  // own unit first
@@ -655,8 +661,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
         const bf16* kp = u == me ? Kin(me) : b.rk[0] + koff;
         const bf16* vp = u == me ? Vin(me) : b.rv[0] + koff;
-        if (qj != me) CK(cudaStreamWaitEvent(st, sev[qj], 0));
-        if (u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
+        if (ctx->ipc && qj != me) CK(cudaStreamWaitEvent(st, sev[qj], 0));
+        if (ctx->ipc && u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
         FwdArgs fa{};
         fa.nq = g.n;
         fa.nk = g.n;
@@ -679,6 +685,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         prof_end(ctx, st, e0, ctx->ev_fwd);
       }
     }
+    }  // ranks
   } else {
     // Alg. 1 l.1: team all-gather (member-major).
     if (C > 1) {
@@ -909,14 +916,14 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto pdq = [&](int r, int s) -> float* { return lp(r, B(ctx, r).pdq[s & 1]); };
   std::vector<int> pkg_team(P);
   for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
-  const bool unitpipe = ctx->ipc && !g.paper && C > 1;
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && !g.paper && C > 1;
   if (unitpipe) {
     // Extension regime over peer memory (R = 1): unit-pipelined like the forward.  The
     // gathers of Q, dO, LSE, D and the K/V slice pull run on the comm stream with one
     // completion event per source rank; the step is cut into (query unit, key unit)
     // launches, locally present units first.  dQ rows accumulate per query unit, dK/dV
-    // rows per key unit.
-    const int me = ctx->rank, t = me / C, a = me % C;
+    // rows per key unit.  (Emulated mode can run the same decomposition for every
+    // virtual rank, WF_EMU_UNITPIPE=1, so it is tested at every (P, C) on one GPU.)
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));  // after D of my rows
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
@@ -944,7 +951,13 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         xs.push_back(x);
       }
     }
-    WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    if (ctx->ipc)
+      WCK(run_phase_per_source(ctx, xs, tr, ctx->comm_stream, sev));
+    else
+      WCK(run_phase(ctx, xs, tr, st));
+    for (int me = 0; me < P; ++me) {
+    if (!local(ctx, me)) continue;
+    const int t = me / C, a = me % C;
     RankBufs& b = B(ctx, me);
     CK(cudaMemsetAsync(b.pdq[0], 0, team * 4, st));
     std::vector<int> qorder, korder;
@@ -964,8 +977,8 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
         const bf16* kp = u == me ? L(me, K, n * E) : b.rk[0] + koff;
         const bf16* vp = u == me ? L(me, V, n * E) : b.rv[0] + koff;
-        if (!own) CK(cudaStreamWaitEvent(st, sev[qj], 0));
-        if (u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
+        if (ctx->ipc && !own) CK(cudaStreamWaitEvent(st, sev[qj], 0));
+        if (ctx->ipc && u != me) CK(cudaStreamWaitEvent(st, sev[u], 0));
         BwdArgs ba{};
         ba.nq = g.n;
         ba.nk = g.n;
@@ -991,6 +1004,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         prof_end(ctx, st, e0, ctx->ev_bwd);
       }
     }
+    }  // ranks
   } else {
     // team gathers: Q + dO, LSE + D, and (paper regime) K + V
     if (C > 1) {
@@ -1315,6 +1329,8 @@ wf_status wf_init_emulated(int P, int C, wf_ctx** out) {
   wf_ctx* tmp = nullptr;
   WCK(new_ctx(P, C, &ctx, &tmp));
   ctx->emulated = true;
+  const char* up = std::getenv("WF_EMU_UNITPIPE");
+  ctx->emu_unitpipe = up && up[0] == '1';
   wf_status s = make_streams(ctx);
   if (s != WF_OK) {
     g_ctxless_err = ctx->err;

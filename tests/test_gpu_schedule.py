@@ -94,3 +94,17 @@ def test_emulated_dit_shape():
     inputs, outs, _ = run_path(4, 2, 1024, 3, 72, False, seed=7)
     ok, errs = check_values(inputs, outs, False)
     assert ok, errs
+
+
+@pytest.mark.parametrize("P,C", [(2, 2), (4, 4), (8, 4)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_emulated_unit_pipelined_extension(P, C, causal, monkeypatch):
+    # the real-mode decomposition of the extension regime (one launch per (query unit, key
+    # unit), W = P / C key units per slice; W = 2 at P = 8, C = 4), run for every virtual rank
+    monkeypatch.setenv("WF_EMU_UNITPIPE", "1")
+    N = 256 * P if causal else 128 * P * 2
+    h, d = 2, 128
+    inputs, outs, trace = run_path(P, C, N, h, d, causal, seed=P + C + 1)
+    ok, errs = check_values(inputs, outs, causal)
+    assert ok, (P, C, causal, errs)
+    assert Counter(trace) == oracle_trace(P, C, N, h, d, causal)
