@@ -196,7 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_s = [&](int i) {
         const int st = i % QST;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
+        tl_stamp(a.tl, tlon, 0, i, 4);
         mbar_wait(&bar[B_QF + st], (i / QST) & 1);
+        tl_stamp(a.tl, tlon, 0, i, 5);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
@@ -214,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = ii % QST;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
         // dP^T = V dO^T (the dP region must be drained of the previous dQ)
+        tl_stamp(a.tl, tlon, 0, ii, 6);
         mbar_wait(&bar[B_DOF], ii & 1);
+        tl_stamp(a.tl, tlon, 0, ii, 7);
         if (ii >= 1) mbar_wait(&bar[B_DQE], (ii - 1) & 1);
         tc_fence_after();
         tl_stamp(a.tl, tlon, 0, ii, 0);
