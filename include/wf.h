@@ -186,6 +186,11 @@ wf_status wf_block_fwd(const void* q, const void* k, const void* v, int nq, int 
  * A bf16 [M, K], B bf16 [N, K], Y bf16 [M, N], all row-major, fp32 accumulation.
  * M multiple of 128, N of 128, K of 64 (WF_ERR_CONFIG otherwise); 16-byte aligned. */
 wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* Y, void* stream);
+/* General layouts: Y[m, n] = sum_k A(m, k) B(n, k) with A stored [M, K] (a_mn = 0) or
+ * [K, M] (a_mn = 1), B stored [N, K] (b_mn = 0) or [K, N] (b_mn = 1): the backward
+ * products dX = dY W (a_mn 0, b_mn 1) and dW = dY^T X (a_mn 1, b_mn 1) of a projection. */
+wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int b_mn, int M, int N, int K, void* Y,
+                         void* stream);
 
 /* wf_block_bwd: PAPER.md:203 one flash-attention backward step: the K/V block
  * (stationary) against query rows q with dO, final LSE and D = rowsum(dO o O) [heads, nq].

@@ -35,6 +35,7 @@ _SIGS = {
     "wf_attn_fwd": (c_int, [c_p, c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_p, c_p, c_p]),
     "wf_qkv_proj": (c_int, [c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
     "wf_gemm_bf16": (c_int, [c_p, c_p, c_int, c_int, c_int, c_p, c_p]),
+    "wf_gemm_bf16_t": (c_int, [c_p, c_int, c_p, c_int, c_int, c_int, c_int, c_p, c_p]),
     "wf_attn_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
     "wf_get_trace": (c_int, [c_p, ctypes.POINTER(WfEvent), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "wf_plan_trace": (c_int, [c_int, c_int, c_i64, c_int, c_int, c_int, ctypes.POINTER(WfEvent), ctypes.c_size_t,

@@ -199,7 +199,8 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
   return WF_OK;
 }
 
-extern "C" wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* Y, void* stream) {
+extern "C" wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int b_mn, int M, int N, int K, void* Y,
+                                    void* stream) {
   if (!A || !B || !Y) return set_err(WF_ERR_ARG, "wf_gemm_bf16: null pointer");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Y)) & 15)
     return set_err(WF_ERR_ARG, "wf_gemm_bf16: pointers must be 16-byte aligned");
@@ -207,8 +208,9 @@ extern "C" wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, in
     return set_err(WF_ERR_CONFIG, "wf_gemm_bf16: M, N multiples of 128 and K of 64 required");
   const int bn = N % 256 == 0 ? 256 : 128;
   CUtensorMap ta, tb;
-  if (!make_tmap_2d(&ta, A, M, K, 128) || !make_tmap_2d(&tb, B, N, K, bn))
-    return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
+  const bool oka = a_mn ? make_tmap_2d(&ta, A, K, M, 64) : make_tmap_2d(&ta, A, M, K, 128);
+  const bool okb = b_mn ? make_tmap_2d(&tb, B, K, N, 64) : make_tmap_2d(&tb, B, N, K, bn);
+  if (!oka || !okb) return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
   GemmArgs g{};
   g.M = M;
   g.N = N;
@@ -217,7 +219,11 @@ extern "C" wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, in
   g.ndst[0] = 1;
   g.ld = N;
   g.out[0][0] = static_cast<__nv_bfloat16*>(Y);
-  cudaError_t e = launch_gemm(ta, tb, g, bn, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_gemm_t(ta, tb, g, bn, a_mn ? 1 : 0, b_mn ? 1 : 0, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
   return WF_OK;
+}
+
+extern "C" wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* Y, void* stream) {
+  return wf_gemm_bf16_t(A, 0, B, 0, M, N, K, Y, stream);
 }

@@ -158,6 +158,9 @@ struct GemmArgs {
   __nv_bfloat16* out[3][WF_GEMM_MAX_DST];
 };
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, cudaStream_t s);
+// a_mn / b_mn: operand stored MN-major ([K, M] / [K, N]); its TMA map has 64 x 64 boxes.
+cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, int a_mn, int b_mn,
+                          cudaStream_t s);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);

@@ -43,7 +43,10 @@ __device__ __forceinline__ void tile_coords(int tile, int nm, int nn, int& m, in
   n = r / rows;
 }
 
-template <int BN>
+// A_MN / B_MN: operand stored MN-major ([K, M] / [K, N] row-major: the transposed operands
+// of the backward GEMMs dX = dY W and dW = dY^T X) instead of K-major ([M, K] / [N, K]).
+// MN-major tiles arrive as 64-column panels of [64 K rows x 128 B] (8 KB), LBO = 8 KB.
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(192, 1)
     wf_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                    const __grid_constant__ GemmArgs g) {
@@ -88,14 +91,23 @@ __global__ void __launch_bounds__(192, 1)
           if (it >= Cfg::ST) mbar_wait(&bar[G_EMPTY + s], ((it / Cfg::ST) - 1) & 1);
           uint8_t* sa = smem + s * Cfg::STAGE;
           mbar_arrive_expect_tx(&bar[G_FULL + s], Cfg::STAGE);
-          tma_load_2d(sa, &tA, &bar[G_FULL + s], kb * 64, m * 128);
-          tma_load_2d(sa + Cfg::A_BYTES, &tB, &bar[G_FULL + s], kb * 64, n * BN);
+          if (A_MN) {
+            for (int p = 0; p < 2; ++p) tma_load_2d(sa + p * 8192, &tA, &bar[G_FULL + s], m * 128 + p * 64, kb * 64);
+          } else {
+            tma_load_2d(sa, &tA, &bar[G_FULL + s], kb * 64, m * 128);
+          }
+          if (B_MN) {
+            for (int p = 0; p < BN / 64; ++p)
+              tma_load_2d(sa + Cfg::A_BYTES + p * 8192, &tB, &bar[G_FULL + s], n * BN + p * 64, kb * 64);
+          } else {
+            tma_load_2d(sa + Cfg::A_BYTES, &tB, &bar[G_FULL + s], kb * 64, n * BN);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN, 0, 0);  // both operands K-major
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
         const int b = lt & 1;
@@ -108,9 +120,11 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * Cfg::STAGE), sb = sa + Cfg::A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(acc, smem_desc_sw128(sa + kk * 32, 16, 1024), smem_desc_sw128(sb + kk * 32, 16, 1024), idesc,
-                   (kb | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t da = A_MN ? smem_desc_sw128(sa + kk * 2048, 8192, 1024) : smem_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? smem_desc_sw128(sb + kk * 2048, 8192, 1024) : smem_desc_sw128(sb + kk * 32, 16, 1024);
+            mma_ss(acc, da, db, idesc, (kb | kk) ? 1u : 0u);
+          }
           mma_commit(&bar[G_EMPTY + s]);
         }
         mma_commit(&bar[G_TFULL + b]);
@@ -185,31 +199,46 @@ int sm_count() {
   return n;
 }
 
-template <int BN>
+template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   using Cfg = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(wf_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(wf_gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int ntiles = (g.M / 128) * (g.N / BN);
   const int grid = ntiles < sm_count() ? ntiles : sm_count();
-  wf_gemm_kernel<BN><<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g);
+  wf_gemm_kernel<BN, A_MN, B_MN><<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g);
   return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_layout(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int a_mn, int b_mn,
+                          cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_bn<BN, false, false>(ta, tb, g, s);
+  if (!a_mn && b_mn) return launch_bn<BN, false, true>(ta, tb, g, s);
+  if (a_mn && b_mn) return launch_bn<BN, true, true>(ta, tb, g, s);
+  return launch_bn<BN, true, false>(ta, tb, g, s);
 }
 
 }  // namespace
 
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, cudaStream_t s) {
+  return launch_gemm_t(ta, tb, g, bn, 0, 0, s);
+}
+
+cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, int a_mn, int b_mn,
+                          cudaStream_t s) {
   if (g.M <= 0 || g.M % 128 || g.K <= 0 || g.K % 64 || g.N <= 0 || g.N % bn || g.split % bn)
     return cudaErrorInvalidValue;
   for (int p = 0; p < 3; ++p)
     if (g.ndst[p] < 0 || g.ndst[p] > WF_GEMM_MAX_DST) return cudaErrorInvalidValue;
   switch (bn) {
-    case 256: return launch_bn<256>(ta, tb, g, s);
-    case 128: return launch_bn<128>(ta, tb, g, s);
+    case 256: return launch_layout<256>(ta, tb, g, a_mn, b_mn, s);
+    case 128: return launch_layout<128>(ta, tb, g, a_mn, b_mn, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -66,12 +66,14 @@ def block_fwd(q, k, v, causal=False, chunk=0, qstart=None, kstart=None, o_in=Non
     return of, ob, lse
 
 
-def gemm_bf16(a, b, y=None):
-    """Y = A B^T on the tensor cores (wf_gemm_bf16): a [M, K], b [N, K] bf16 -> y [M, N] bf16."""
-    M, K = a.shape
-    N = b.shape[0]
+def gemm_bf16(a, b, y=None, a_mn=False, b_mn=False):
+    """Y[m, n] = sum_k A(m, k) B(n, k) on the tensor cores (wf_gemm_bf16_t).
+    a: [M, K] (or [K, M] with a_mn), b: [N, K] (or [K, N] with b_mn), bf16 -> y [M, N] bf16."""
+    M, K = (a.shape[1], a.shape[0]) if a_mn else a.shape
+    N = b.shape[1] if b_mn else b.shape[0]
     y = torch.empty((M, N), dtype=torch.bfloat16, device=a.device) if y is None else y
-    _check(lib().wf_gemm_bf16(_ptr(_bf16(a, "a")), _ptr(_bf16(b, "b")), M, N, K, _ptr(_bf16(y, "y")), _stream()))
+    _check(lib().wf_gemm_bf16_t(_ptr(_bf16(a, "a")), int(a_mn), _ptr(_bf16(b, "b")), int(b_mn), M, N, K,
+                                _ptr(_bf16(y, "y")), _stream()))
     return y
 
 

@@ -41,6 +41,22 @@ def test_gemm_parity(M, N, K):
     assert ok, worst
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 192), (384, 1152, 256)])
+def test_gemm_transposed_layouts(a_mn, b_mn, M, N, K):
+    # the backward products of a projection: dX = dY W (b_mn), dW = dY^T X (a_mn, b_mn)
+    wf = _wf()
+    g = torch.Generator().manual_seed(M + 3 * N + K + a_mn)
+    a = torch.randn((K, M) if a_mn else (M, K), generator=g).to(torch.bfloat16)
+    b = (torch.randn((K, N) if b_mn else (N, K), generator=g) * K ** -0.5).to(torch.bfloat16)
+    y = wf.gemm_bf16(a.cuda(), b.cuda(), a_mn=bool(a_mn), b_mn=bool(b_mn))
+    torch.cuda.synchronize()
+    A = to_f64(a).T if a_mn else to_f64(a)
+    B = to_f64(b).T if b_mn else to_f64(b)
+    ok, worst = _close(to_f64(y), gemm(A, B))
+    assert ok, worst
+
+
 def test_gemm_large_sampled_rows():
     # the GPT-7B projection shape of one rank at P = 8 (16K rows, 4096 -> 3 x 4096)
     wf = _wf()
