@@ -192,6 +192,26 @@ wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* 
 wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int b_mn, int M, int N, int K, void* Y,
                          void* stream);
 
+/* ---- the other operators of a WallFacer Transformer layer (SURVEY.md §8(f) item 3,
+ * the GPT-7B-style block of P:337/P:407, driven by paper_2407_00611_b200/layer.py) ----
+ * All bf16 row-major device buffers, 16-byte aligned; status as above.
+ * wf_rmsnorm_fwd: y = x * rstd * w, rstd[row] = 1/sqrt(mean(x^2) + eps) (fp32 out).
+ * wf_rmsnorm_bwd: dx = rstd (w o dy) - x rstd^3 mean(w o dy o x) (+ dres if non-NULL: the
+ *   residual branch's gradient), dw += sum_rows dy o x rstd (fp32, accumulated: zero it
+ *   first).  hidden <= 8192.
+ * wf_swiglu_fwd: gu = [gate | up] ([rows, 2 ffn]) -> h = silu(gate) o up ([rows, ffn]).
+ * wf_swiglu_bwd: dh -> dgu = [dh o up o silu'(gate) | dh o silu(gate)].
+ * wf_add_bf16: y = a + b (n elements, n % 8 == 0).
+ * wf_pack3_bf16: y [rows, 3E] = [a | b | c] (a, b, c [rows, E]). */
+wf_status wf_rmsnorm_fwd(const void* x, const void* w, int64_t rows, int hidden, float eps, void* y, float* rstd,
+                         void* stream);
+wf_status wf_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dres,
+                         int64_t rows, int hidden, void* dx, float* dw, void* stream);
+wf_status wf_swiglu_fwd(const void* gu, int64_t rows, int ffn, void* h, void* stream);
+wf_status wf_swiglu_bwd(const void* dh, const void* gu, int64_t rows, int ffn, void* dgu, void* stream);
+wf_status wf_add_bf16(const void* a, const void* b, int64_t n, void* y, void* stream);
+wf_status wf_pack3_bf16(const void* a, const void* b, const void* c, int64_t rows, int E, void* y, void* stream);
+
 /* wf_block_bwd: PAPER.md:203 one flash-attention backward step: the K/V block
  * (stationary) against query rows q with dO, final LSE and D = rowsum(dO o O) [heads, nq].
  * dq_acc fp32 [nq, heads, D] is accumulated (+=) atomically; dk_acc/dv_acc fp32

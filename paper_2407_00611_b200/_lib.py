@@ -36,6 +36,12 @@ _SIGS = {
     "wf_qkv_proj": (c_int, [c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
     "wf_gemm_bf16": (c_int, [c_p, c_p, c_int, c_int, c_int, c_p, c_p]),
     "wf_gemm_bf16_t": (c_int, [c_p, c_int, c_p, c_int, c_int, c_int, c_int, c_p, c_p]),
+    "wf_rmsnorm_fwd": (c_int, [c_p, c_p, c_i64, c_int, ctypes.c_float, c_p, c_p, c_p]),
+    "wf_rmsnorm_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_p, c_p, c_p]),
+    "wf_swiglu_fwd": (c_int, [c_p, c_i64, c_int, c_p, c_p]),
+    "wf_swiglu_bwd": (c_int, [c_p, c_p, c_i64, c_int, c_p, c_p]),
+    "wf_add_bf16": (c_int, [c_p, c_p, c_i64, c_p, c_p]),
+    "wf_pack3_bf16": (c_int, [c_p, c_p, c_p, c_i64, c_int, c_p, c_p]),
     "wf_attn_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
     "wf_get_trace": (c_int, [c_p, ctypes.POINTER(WfEvent), ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "wf_plan_trace": (c_int, [c_int, c_int, c_i64, c_int, c_int, c_int, ctypes.POINTER(WfEvent), ctypes.c_size_t,

@@ -98,8 +98,10 @@ static thread_local char g_err[512];
 const char* wf_static_error() { return g_err; }
 static wf_status set_err(wf_status s, const char* msg) {
   std::snprintf(g_err, sizeof(g_err), "%s", msg);
+  wf_clear_ctxless_error();
   return s;
 }
+wf_status wf_set_static_error(wf_status s, const char* msg) { return set_err(s, msg); }
 
 // Debug aid: enable (cta >= 0) / disable (cta < 0) the block-kernel timeline of CTA
 // (cta, head 0); wf_debug_timeline_read copies n words (after a device synchronize).

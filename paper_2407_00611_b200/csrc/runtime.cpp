@@ -1276,6 +1276,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 }  // namespace
 
 // ====================================================================== C ABI
+void wf_clear_ctxless_error() { g_ctxless_err.clear(); }
+
 extern "C" {
 
 wf_status wf_get_uid(wf_uid* out) {

@@ -77,6 +77,53 @@ def gemm_bf16(a, b, y=None, a_mn=False, b_mn=False):
     return y
 
 
+def rmsnorm_fwd(x, w, eps=1e-5, y=None, rstd=None):
+    """y = x rstd w (wf_rmsnorm_fwd); returns (y, rstd fp32 [rows])."""
+    rows, H = x.shape
+    y = torch.empty_like(x) if y is None else y
+    rstd = torch.empty((rows,), dtype=torch.float32, device=x.device) if rstd is None else rstd
+    _check(lib().wf_rmsnorm_fwd(_ptr(_bf16(x, "x")), _ptr(_bf16(w, "w")), rows, H, float(eps), _ptr(y), _ptr(rstd),
+                                _stream()))
+    return y, rstd
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dw, dres=None, dx=None):
+    """dx (+ dres) and dw += (wf_rmsnorm_bwd); dw fp32 [H] accumulates."""
+    rows, H = x.shape
+    dx = torch.empty_like(x) if dx is None else dx
+    _check(lib().wf_rmsnorm_bwd(_ptr(_bf16(dy, "dy")), _ptr(x), _ptr(w), _ptr(rstd), _ptr(dres), rows, H, _ptr(dx),
+                                _ptr(dw), _stream()))
+    return dx
+
+
+def swiglu_fwd(gu, h=None):
+    rows, F2 = gu.shape
+    h = torch.empty((rows, F2 // 2), dtype=torch.bfloat16, device=gu.device) if h is None else h
+    _check(lib().wf_swiglu_fwd(_ptr(_bf16(gu, "gu")), rows, F2 // 2, _ptr(h), _stream()))
+    return h
+
+
+def swiglu_bwd(dh, gu, dgu=None):
+    rows, F2 = gu.shape
+    dgu = torch.empty_like(gu) if dgu is None else dgu
+    _check(lib().wf_swiglu_bwd(_ptr(_bf16(dh, "dh")), _ptr(gu), rows, F2 // 2, _ptr(dgu), _stream()))
+    return dgu
+
+
+def add_bf16(a, b, y=None):
+    y = torch.empty_like(a) if y is None else y
+    _check(lib().wf_add_bf16(_ptr(_bf16(a, "a")), _ptr(_bf16(b, "b")), a.numel(), _ptr(y), _stream()))
+    return y
+
+
+def pack3(a, b, c, y=None):
+    rows = a.shape[0]
+    E = a.numel() // rows
+    y = torch.empty((rows, 3 * E), dtype=torch.bfloat16, device=a.device) if y is None else y
+    _check(lib().wf_pack3_bf16(_ptr(_bf16(a, "a")), _ptr(b), _ptr(c), rows, E, _ptr(y), _stream()))
+    return y
+
+
 def block_bwd(q, k, v, do, lse, dsum, dq_acc, dk_acc, dv_acc, causal=False, chunk=0, qstart=None, kstart=None,
               accumulate=False):
     """One flash-attention backward step on the current device (in place on the accumulators)."""
