@@ -128,3 +128,29 @@ def test_error_paths():
     ctx.close()
     with pytest.raises(wf.WFError, match="status 2"):  # C does not divide P
         wf.Context(8, 3, emulated=True)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N", [262144, 524288])
+def test_max_length_sampled(N):
+    # the longest BASELINE sequence lengths on one GPU (2^31 elements per tensor at 512K):
+    # sampled query rows of two heads against the oracle, and the dV column-sum identity
+    wf = _wf()
+    h, d = 32, 128
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, do = (torch.randn((N, h, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    ctx = wf.Context(1, 1)
+    o, lse = ctx.fwd(q, k, v, N, True)
+    dq, dk, dv = ctx.bwd(do, q, k, v, o, lse, N, True)
+    torch.cuda.synchronize()
+    ctx.close()
+    rows = np.array([0, 777, N // 2 + 5, N - 1])
+    for hh in (0, h - 1):
+        K, V = to_f64(k[:, hh:hh + 1].cpu()), to_f64(v[:, hh:hh + 1].cpu())
+        Q = to_f64(q[rows, hh:hh + 1].cpu())
+        o_ref, l_ref = attention_fwd(Q, K, V, qpos=rows, kpos=np.arange(N), causal=True)
+        assert np.abs(to_f64(o[rows, hh:hh + 1].cpu()) - o_ref).max() <= 2e-2
+        assert np.abs(lse[hh, rows].double().cpu().numpy() - l_ref[0]).max() <= 1e-2
+    s_dv = dv.float().sum(0)
+    s_do = do.float().sum(0)
+    assert (s_dv - s_do).abs().max().item() <= 2e-3 * do.float().abs().sum(0).max().item()
