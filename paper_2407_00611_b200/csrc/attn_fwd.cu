@@ -26,7 +26,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef WF_POLY_EVERY
-#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU)
+#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU); 4 saves 1.5 % (GPT) / 3.6 % (DiT) of fwd time but moved one peaky parity case from 0.019 to 0.023 max |dO|: off
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 16; ++i) {
             const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
 #if WF_POLY_EVERY > 0
-            const bool poly = ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
+            // masked (-inf) logits exist only on DIAG tiles: those stay on MUFU (exact 0)
+            const bool poly = !DIAG && ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
             const float2 p = poly ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
 #else
             const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
