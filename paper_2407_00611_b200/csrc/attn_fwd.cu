@@ -26,7 +26,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef WF_POLY_EVERY
-#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU); 4 saves 1.5 % (GPT) / 3.6 % (DiT) of fwd time but moved one peaky parity case from 0.019 to 0.023 max |dO|: off
+#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU); 4 saves 1.5 % (GPT) / 3.6 % (DiT) of fwd time but pushed one peaky parity case past the 2e-2 O bound (0.023): off
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
 
