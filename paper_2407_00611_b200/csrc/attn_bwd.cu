@@ -45,7 +45,7 @@ struct BwdCfg {
 
 enum {
   B_KV = 0, B_QF = 1, B_QE = 4, B_SF = 7, B_SE = 9, B_DOF = 11, B_DOE = 12, B_S = 13, B_DP = 14, B_P = 15,
-  B_DS = 16, B_DQF = 17, B_DQE = 18, B_DSE = 19, B_DONE = 20, B_NUM = 21
+  B_DS = 16, B_DQF = 17, B_DQE = 18, B_DSE = 19, B_DONE = 20, B_SL = 21, B_SRF = 22, B_NUM = 23
 };
 
 #ifndef WF_BWD_POLY_EVERY
@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ BwdArgs a) {
   using Cfg = BwdCfg<D>;
   constexpr int DP = Cfg::DP;
+#ifndef WF_BWD_PARK
+#define WF_BWD_PARK 1
+#endif
+  constexpr bool kPark = WF_BWD_PARK && DP > 64;  // park dQ's second half in free S^T columns
   constexpr int QST = Cfg::QST;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -125,6 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar[B_DQE], 128);
     mbar_init(&bar[B_DSE], 1);
     mbar_init(&bar[B_DONE], 1);
+    mbar_init(&bar[B_SL], kCompute);
+    mbar_init(&bar[B_SRF], 128);
     fence_barrier_init();
   }
   if (warp == 13) {
@@ -197,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = i % QST;
         const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
         tl_stamp(a.tl, tlon, 0, i, 4);
+        if (kPark && i >= 2) mbar_wait(&bar[B_SRF], (i - 2) & 1);  // drain of tile i-2 left S^T columns [64, 128)
         mbar_wait(&bar[B_QF + st], (i / QST) & 1);
         tl_stamp(a.tl, tlon, 0, i, 5);
         tc_fence_after();
@@ -289,11 +296,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 0);
       uint32_t pk[32];  // P^T row, this half: 64 bf16
+      uint32_t sv[2][32];
+      tmem_ld32(tl + hf * 64, sv[0]);
+      tmem_ld32(tl + hf * 64 + 32, sv[1]);
+      tmem_wait_ld();
+      // all of S^T is in registers: P may now overwrite columns [0, 64) (after both halves
+      // have loaded: the named barrier), and the dQ drain may park data in [64, 128)
+      tc_fence_before();
+      mbar_arrive(&bar[B_SL]);
+      named_bar_sync(3, kCompute);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(tl + hf * 64 + c * 32, rr);
-        tmem_wait_ld();
+        const uint32_t* rr = sv[c];
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
         if (kind == 2) {  // diagonal tile: key r is visible to query column q iff r <= q
 #pragma unroll
@@ -429,42 +443,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = warp * 32 + lane;  // query row within the tile
     const uint32_t tl = tbase + (static_cast<uint32_t>(warp * 32) << 16);
     uint8_t* wbox0 = smem + Cfg::OFF_STG + warp * 8192;
+    const int ntiles = q_iter().count(a.qpos);
     int ii = 0, chunk = 0;
     int it, qp;
+    // read columns [cb, cb + 64) (clipped to DP) of the TMEM address base into ra / rb
+    auto ld_half = [&](uint32_t base, int cb, uint32_t(&ra)[32], uint32_t(&rb)[32]) {
+      if (cb + 32 <= DP) {
+        tmem_ld32(base, ra);
+      } else {
+        uint32_t r16[16];
+        tmem_ld16(base, r16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ra[i] = r16[i];
+#pragma unroll
+        for (int i = 16; i < 32; ++i) ra[i] = 0u;
+      }
+      if (cb + 32 < DP) {
+        if (cb + 64 <= DP) {
+          tmem_ld32(base + 32, rb);
+        } else {
+          uint32_t r16[16];
+          tmem_ld16(base + 32, r16);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) rb[i] = r16[i];
+#pragma unroll
+          for (int i = 16; i < 32; ++i) rb[i] = 0u;
+        }
+      }
+    };
     for (auto iq = q_iter(); iq.next(a.qpos, it, qp);) {
       mbar_wait(&bar[B_DQF], ii & 1);
       tc_fence_after();
       tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 0);
+      // Park the second half of dQ in the free columns [64, 128) of the S^T region (the
+      // compute warps hold S^T of the next tile in registers by then), so the dP/dQ region
+      // is released after two TMEM reads instead of after staging the first half.
+      const bool park = kPark && ii + 1 < ntiles;
+      if (park) {
+        mbar_wait(&bar[B_SL], (ii + 1) & 1);
+        tc_fence_after();
+        uint32_t ra[32], rb[32];
+        ld_half(tl + 256 + 64, 64, ra, rb);
+        tmem_wait_ld();
+        tmem_st32(tl + 64, ra);
+        if (DP > 96) tmem_st32(tl + 96, rb);
+      }
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int cbase = half * 64;
         if (cbase < DP) {
           uint32_t ra[32], rb[32];
           const bool two = cbase + 32 < DP;
-          if (cbase + 32 <= DP) {
-            tmem_ld32(tl + 256 + cbase, ra);
-          } else {
-            uint32_t r16[16];
-            tmem_ld16(tl + 256 + cbase, r16);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) ra[i] = r16[i];
-#pragma unroll
-            for (int i = 16; i < 32; ++i) ra[i] = 0u;
-          }
-          if (two) {
-            if (cbase + 64 <= DP) {
-              tmem_ld32(tl + 256 + cbase + 32, rb);
-            } else {
-              uint32_t r16[16];
-              tmem_ld16(tl + 256 + cbase + 32, r16);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) rb[i] = r16[i];
-#pragma unroll
-              for (int i = 16; i < 32; ++i) rb[i] = 0u;
-            }
-          }
+          ld_half(half == 1 && park ? tl + 64 : tl + 256 + cbase, cbase, ra, rb);
           tmem_wait_ld();
-          if (cbase + 64 >= DP) {  // last TMEM read of this tile: release the dQ region
+          if (half == 0 && park) {  // both halves are out of the dP/dQ region
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bar[B_DQE]);
+            tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 1);
+          } else if (half == 1 && park) {  // parked half read back: S^T columns free again
+            tc_fence_before();
+            mbar_arrive(&bar[B_SRF]);
+          } else if (cbase + 64 >= DP) {  // last TMEM read of this tile: release the dQ region
             tc_fence_before();
             mbar_arrive(&bar[B_DQE]);
             tl_stamp(a.tl, tlon && threadIdx.x == 0, 2, ii, 1);
