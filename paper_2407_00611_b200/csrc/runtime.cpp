@@ -1112,6 +1112,10 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         a.dk_acc = b.dk_acc;
         a.dv_acc = b.dv_acc;
         a.dkv_accumulate = s > 0;
+        if (P == 1) {  // one stationary block that is the whole K/V: write bf16 dK/dV directly
+          a.dk_out = dK;
+          a.dv_out = dV;
+        }
         if (ctx->dry) continue;
         CUtensorMap tq, tk, tv, tdo;
         if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
@@ -1239,6 +1243,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     const std::vector<const float*>* parts[3] = {&qparts[r], &kparts[r], &vparts[r]};
     bf16* outs[3] = {L(r, dQ, n * E), L(r, dK, n * E), L(r, dV, n * E)};
     for (int i = 0; i < 3; ++i) {
+      if (P == 1 && i > 0) continue;  // dK/dV came out of the block kernel in bf16
       SumArgs s{};
       s.n = n * E;
       s.nparts = static_cast<int>(parts[i]->size());
