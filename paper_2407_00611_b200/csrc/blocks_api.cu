@@ -209,10 +209,6 @@ extern "C" wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int 
   if (M <= 0 || M % 128 || N <= 0 || N % 128 || K <= 0 || K % 64)
     return set_err(WF_ERR_CONFIG, "wf_gemm_bf16: M, N multiples of 128 and K of 64 required");
   const int bn = N % 256 == 0 ? 256 : 128;
-  CUtensorMap ta, tb;
-  const bool oka = a_mn ? make_tmap_2d(&ta, A, K, M, 64) : make_tmap_2d(&ta, A, M, K, 128);
-  const bool okb = b_mn ? make_tmap_2d(&tb, B, K, N, 64) : make_tmap_2d(&tb, B, N, K, bn);
-  if (!oka || !okb) return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
   GemmArgs g{};
   g.M = M;
   g.N = N;
@@ -221,7 +217,13 @@ extern "C" wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int 
   g.ndst[0] = 1;
   g.ld = N;
   g.out[0][0] = static_cast<__nv_bfloat16*>(Y);
-  cudaError_t e = launch_gemm_t(ta, tb, g, bn, a_mn ? 1 : 0, b_mn ? 1 : 0, static_cast<cudaStream_t>(stream));
+  const bool pair = gemm_pair_ok(g, a_mn, b_mn);
+  CUtensorMap ta, tb;
+  const bool oka = a_mn ? make_tmap_2d(&ta, A, K, M, 64) : make_tmap_2d(&ta, A, M, K, 128);
+  const bool okb = b_mn ? make_tmap_2d(&tb, B, K, N, 64) : make_tmap_2d(&tb, B, N, K, pair ? 128 : bn);
+  if (!oka || !okb) return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
+  cudaError_t e = pair ? launch_gemm_pair(ta, tb, g, static_cast<cudaStream_t>(stream))
+                       : launch_gemm_t(ta, tb, g, bn, a_mn ? 1 : 0, b_mn ? 1 : 0, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
   return WF_OK;
 }

@@ -161,6 +161,10 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 // a_mn / b_mn: operand stored MN-major ([K, M] / [K, N]); its TMA map has 64 x 64 boxes.
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, int a_mn, int b_mn,
                           cudaStream_t s);
+// CTA-pair (cta_group::2) variant for K-major A and B with M, N, split multiples of 256
+// (WF_GEMM_PAIR=0 disables it); its A and B maps both use 128-row boxes.
+bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn);
+cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);

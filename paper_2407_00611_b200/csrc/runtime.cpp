@@ -1376,8 +1376,14 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int P = g.P, C = g.C;
   const int bn = E % 256 == 0 ? 256 : 128;
+  GemmArgs shape{};
+  shape.M = static_cast<int>(n);
+  shape.N = static_cast<int>(3 * E);
+  shape.split = static_cast<int>(E);
+  const bool pair = gemm_pair_ok(shape, 0, 0);
   CUtensorMap tw;
-  if (!make_tmap_2d(&tw, W, 3 * E, hidden, bn)) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
+  if (!make_tmap_2d(&tw, W, 3 * E, hidden, pair ? 128 : bn))
+    return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
   // fused gather: the epilogue writes straight into the team buffers (peer memory or, emulated,
   // the virtual ranks' workspaces); the NCCL transport keeps the separate gather.
   bool fuse = C > 1 && (ctx->emulated || ctx->ipc) && !(ctx->debug & WF_DEBUG_NO_TRANSFER);
@@ -1427,7 +1433,7 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
     CUtensorMap tx;
     if (!make_tmap_2d(&tx, static_cast<const bf16*>(X) + ro * n * hidden, n, hidden, 128))
       return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
-    WCK(kcheck(ctx, launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
+    WCK(kcheck(ctx, pair ? launch_gemm_pair(tx, tw, ga, st) : launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
   }
   if (fuse) {
     ctx->proj_q = Q;
