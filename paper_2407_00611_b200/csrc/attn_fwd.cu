@@ -411,6 +411,15 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s) {
   if (a.nq <= 0 || a.nq % WF_TILE || a.nk % WF_TILE) return cudaErrorInvalidValue;
+  if (a.kbase && a.nk > 0 && block_fwd_pair_ok(a, D)) {
+    CUtensorMap tk64;
+    if (make_tmap_rows_box(&tk64, a.kbase, a.nk, a.heads, D, 64)) {
+      FwdArgs b = a;
+      b.tl = timeline_buffer();
+      b.tl_cta = timeline_cta();
+      return launch_block_fwd_pair(tq, tk64, tv, b, s);
+    }
+  }
   switch (D) {
     case 128: return launch_fwd_d<128>(tq, tk, tv, a, s);
     case 64: return launch_fwd_d<64>(tq, tk, tv, a, s);

@@ -30,11 +30,15 @@ EncodeFn get_encode() {
 }  // namespace
 
 bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D) {
+  return make_tmap_rows_box(map, base, rows, heads, D, WF_TILE);
+}
+
+bool make_tmap_rows_box(CUtensorMap* map, const void* base, int64_t rows, int heads, int D, int box_rows) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(heads) * D * 2};
-  cuuint32_t box[3] = {64, 1, WF_TILE};
+  cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -154,6 +158,7 @@ extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, i
   a.o_out_bf16 = static_cast<__nv_bfloat16*>(o_bf16);
   a.lse_out = lse_out;
   a.lse_blk = nq;
+  a.kbase = k;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_rows(&tq, q, nq, heads, head_dim) || !make_tmap_rows(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim) ||
       !make_tmap_rows(&tv, v, nk > 0 ? nk : WF_TILE, heads, head_dim))

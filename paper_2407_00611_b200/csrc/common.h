@@ -108,6 +108,7 @@ struct FwdArgs {
   int lse_blk;                    // lse layout: rows in blocks of lse_blk, [nq/blk][heads][blk]
   unsigned long long* tl;         // debug timeline (null = off), see wf_debug_timeline
   int tl_cta;
+  const void* kbase;              // K rows (for the CTA-pair kernel's 64-row key boxes; may be null)
 };
 
 // Arguments of one block-backward launch (flash-attention backward):
@@ -133,6 +134,8 @@ struct BwdArgs {
 
 // Host: encode a 3-D TMA map over a [rows, heads, D] bf16 tensor, box {64, 1, 128}, SW128.
 bool make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int heads, int D);
+// same with a {64, 1, box_rows} box
+bool make_tmap_rows_box(CUtensorMap* map, const void* base, int64_t rows, int heads, int D, int box_rows);
 // Debug timeline (bench/profiling aid): when enabled, one CTA of every block kernel records
 // clock64() stamps at slot ((role * WF_TL_TILES + tile) * 8 + event).
 #define WF_TL_TILES 1024
@@ -168,6 +171,10 @@ cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
+// CTA-pair forward (attn_fwd2.cu): head_dim 128, nq % 512 == 0, opt-in with WF_FWD_PAIR=1
+bool block_fwd_pair_ok(const FwdArgs& a, int D);
+cudaError_t launch_block_fwd_pair(const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,
+                                  const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                              const CUtensorMap& tdo, const BwdArgs& a, int D, cudaStream_t s);
 

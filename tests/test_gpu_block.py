@@ -129,3 +129,38 @@ def test_block_bwd(causal, d):
     for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
         errs[name] = np.abs(got.cpu().double().numpy() - ref).max() / max(np.abs(ref).max(), 1e-30)
     assert max(errs.values()) <= G_TOL, errs
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("case", ["contiguous", "zigzag", "state"])
+def test_block_fwd_cta_pair(causal, case, monkeypatch):
+    """The opt-in CTA-pair forward (attn_fwd2.cu, WF_FWD_PAIR=1): query rows in whole pairs of
+    pairs (nq % 512 == 0), contiguous and zigzag chunks, with and without an incoming state."""
+    monkeypatch.setenv("WF_FWD_PAIR", "1")
+    wf = _wf()
+    h, d = 2, 128
+    if case == "contiguous":
+        o, l, o_ref, l_ref = _run_fwd(1024, 1024, h, d, causal, 1024, [0], [0], peaky=True)
+    elif case == "zigzag":
+        o, l, o_ref, l_ref = _run_fwd(1024, 1024, h, d, causal, 256, [0, 1792, 512, 1280], [256, 1536, 768, 1024],
+                                      peaky=True)
+    else:
+        n = 512
+        q, k, v, _ = make_qkv_do(3 * n, h, d, seed=5, peaky=True)
+        qd = q[:n].cuda()
+        qstart = [1024, 256]
+        blocks = [([0, 512], k[:n], v[:n]), ([768, 1280], k[n:2 * n], v[n:2 * n])]
+        of, lse = None, None
+        for i, (ks, kb, vb) in enumerate(blocks):
+            last = i == len(blocks) - 1
+            of2, ob, lse2 = wf.block_fwd(qd, kb.cuda(), vb.cuda(), causal=causal, chunk=256, qstart=qstart, kstart=ks,
+                                         o_in=of, lse_in=lse, out_f32=not last, out_bf16=last)
+            of, lse = of2, lse2
+        torch.cuda.synchronize()
+        qp = _pos(256, qstart) if causal else np.arange(n)
+        kp = np.concatenate([_pos(256, b[0]) for b in blocks]) if causal else np.arange(2 * n)
+        o_ref, l_ref = attention_fwd(to_f64(q[:n]), to_f64(torch.cat([b[1] for b in blocks])),
+                                     to_f64(torch.cat([b[2] for b in blocks])), qp, kp, causal)
+        o, l = to_f64(ob), lse.cpu().double().numpy()
+    eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
