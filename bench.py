@@ -124,16 +124,21 @@ def cpu_oracle_sample(N_s, heads_s, hd, causal):
     """Time the fp64 oracle (dense fwd+bwd) on a bounded sample; returns (TFLOP/s, seconds, cores)."""
     import numpy as np
     from oracle.dense import attention_bwd
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([t.get("num_threads", 1) for t in threadpool_info() if t.get("user_api") == "blas"] or [1])
-    except Exception:
-        cores = os.cpu_count()
     rng = np.random.default_rng(0)
     q, k, v, do = (rng.standard_normal((N_s, heads_s, hd)) for _ in range(4))
-    t0 = time.perf_counter()
-    attention_bwd(q, k, v, do, causal=causal)
-    dt = time.perf_counter() - t0
+    try:
+        # the host's cores (torchrun sets OMP_NUM_THREADS=1 for its workers)
+        from threadpoolctl import threadpool_info, threadpool_limits
+        with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+            cores = max([t.get("num_threads", 1) for t in threadpool_info() if t.get("user_api") == "blas"] or [1])
+            t0 = time.perf_counter()
+            attention_bwd(q, k, v, do, causal=causal)
+            dt = time.perf_counter() - t0
+    except ImportError:
+        cores = os.cpu_count()
+        t0 = time.perf_counter()
+        attention_bwd(q, k, v, do, causal=causal)
+        dt = time.perf_counter() - t0
     f, b = flops(N_s, heads_s, hd, causal)
     return (f + b) / dt / 1e12, dt, cores
 
