@@ -131,6 +131,20 @@ wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int ra
  * bytes is null. */
 wf_status wf_workspace_bytes(int P, int C, int64_t N, int heads, int head_dim, int causal, size_t* bytes);
 
+/* Schedule variants (SURVEY.md §8(a) "Schedule variants", reading c21).  Both compute the
+ * same result; they differ in how the paper regime's first K/V block reaches a rank:
+ * WF_SCHED_GATHER_SHUFFLE (default, the paper's Alg. 1 l.1-2): team all-gather of K/V,
+ * then the init shuffle of the team block to init_send (AG_KV + INIT_KV messages);
+ * WF_SCHED_DIRECT_PULL: every unit of the block team(init_recv) comes straight from its
+ * owner (SLICE_KV messages, as in the extension regime), one hop instead of two; with
+ * R = 1 the step is then unit-pipelined like the extension regime.  Set before the first
+ * wf_attn_fwd of a shape; the extension regime and C = 1 are unaffected. */
+#define WF_SCHED_GATHER_SHUFFLE 0
+#define WF_SCHED_DIRECT_PULL 1
+wf_status wf_set_schedule(wf_ctx* ctx, int sched);
+wf_status wf_plan_trace_sched(int P, int C, int64_t N, int heads, int head_dim, int rank, int sched, wf_event* buf,
+                              size_t cap, size_t* n_out);
+
 /* Host-only: the plan of one rank: out[0..5] = {init_send, init_recv, next, last, R, regime}
  * (regime 0 = paper, 1 = extension). */
 wf_status wf_plan(int P, int C, int rank, int32_t out[6]);

@@ -85,8 +85,13 @@ def _rows_of_member(arr, j, n):
     return arr[j * n:(j + 1) * n]
 
 
-def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=None, net=None):
+def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=None, net=None, direct=False):
     """Q/K/V: global [N, h, d] float64 (or None with compute=False).
+
+    direct: the DIRECT-PULL init variant (SURVEY.md §8(a) "Schedule variants", reading
+    c21): in the paper regime the K/V team all-gather and the init shuffle are replaced by
+    one message per unit from its owner to every rank whose initial block contains it
+    (kind SLICE_KV, as in the extension regime); the ring itself is unchanged.
 
     Returns (O [N,h,d], LSE [h,N], events, ctx) -- outputs in global token order.
     """
@@ -107,7 +112,7 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
         t = r // C
         for p in range(t * C, t * C + C):
             net.send(0, "AG_Q", -1, r, p, r, n * E * 2, local[r][0] if compute else None)
-            if plan["regime"] == "paper":
+            if plan["regime"] == "paper" and not direct:
                 net.send(0, "AG_KV", -1, r, p, r, 2 * n * E * 2, local[r][1:] if compute else None)
     team = {}
     for r in range(P):
@@ -117,7 +122,7 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
         for p in members:
             _, q = net.recv("AG_Q", -1, p, r)
             qs.append(q)
-            if plan["regime"] == "paper":
+            if plan["regime"] == "paper" and not direct:
                 _, kv = net.recv("AG_KV", -1, p, r)
                 kvs.append(kv)
         entry = dict(qpos=team_positions(members, P, N, causal))
@@ -131,15 +136,27 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
     partial = {}
     if plan["regime"] == "paper":
         send, recv, nxt, lst = plan["send"], plan["recv"], plan["next"], plan["last"]
-        # Alg. 1 l.2: init shuffle of the team K/V block.
-        for r in range(P):
-            t = r // C
-            kv = (team[r]["k"], team[r]["v"]) if compute else None
-            net.send(0, "INIT_KV", -1, r, send[r], t, 2 * C * n * E * 2, kv)
         cur = {}
-        for r in range(P):
-            blk, kv = net.recv("INIT_KV", -1, recv[r], r)
-            cur[r] = (blk, kv)
+        if direct:
+            # the units of the initial block team(recv[r]) straight from their owners
+            for r in range(P):
+                blk = recv[r] // C
+                for u in range(blk * C, blk * C + C):
+                    net.send(0, "SLICE_KV", -1, u, r, u, 2 * n * E * 2, local[u][1:] if compute else None)
+            for r in range(P):
+                blk = recv[r] // C
+                kvs = [net.recv("SLICE_KV", -1, u, r)[1] for u in range(blk * C, blk * C + C)]
+                kv = ((np.concatenate([x[0] for x in kvs]), np.concatenate([x[1] for x in kvs])) if compute else None)
+                cur[r] = (blk, kv)
+        else:
+            # Alg. 1 l.2: init shuffle of the team K/V block.
+            for r in range(P):
+                t = r // C
+                kv = (team[r]["k"], team[r]["v"]) if compute else None
+                net.send(0, "INIT_KV", -1, r, send[r], t, 2 * C * n * E * 2, kv)
+            for r in range(P):
+                blk, kv = net.recv("INIT_KV", -1, recv[r], r)
+                cur[r] = (blk, kv)
         state = {r: (init_state(C * n, h, d) if compute else None) for r in range(P)}
         for s in range(R):                                         # Alg. 1 l.5
             for r in range(P):
@@ -197,8 +214,10 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
     return O, LSE, net.events, dict(plan=plan, n=n, E=E)
 
 
-def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=None, head_dim=None, net=None):
+def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=None, head_dim=None, net=None,
+                      direct=False):
     """Backward of the schedule.  O, LSE: final forward outputs (global order).
+    direct: the DIRECT-PULL init variant (see simulate_forward) for the stationary block.
 
     Returns (dQ, dK, dV, events).
     """
@@ -228,7 +247,7 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
             x = loc[r]
             net.send(1, "AG_QDO", -1, r, p, r, 2 * n * E * 2, (x["q"], x["do"]) if compute else None)
             net.send(1, "AG_STATS", -1, r, p, r, 2 * n * h * 4, (x["lse"], x["dd"]) if compute else None)
-            if plan["regime"] == "paper":
+            if plan["regime"] == "paper" and not direct:
                 net.send(1, "AG_KV", -1, r, p, r, 2 * n * E * 2, (x["k"], x["v"]) if compute else None)
     team = {}
     for r in range(P):
@@ -236,7 +255,7 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
         members = list(range(t * C, t * C + C))
         qd = [net.recv("AG_QDO", -1, p, r)[1] for p in members]
         st = [net.recv("AG_STATS", -1, p, r)[1] for p in members]
-        kv = [net.recv("AG_KV", -1, p, r)[1] for p in members] if plan["regime"] == "paper" else []
+        kv = [net.recv("AG_KV", -1, p, r)[1] for p in members] if plan["regime"] == "paper" and not direct else []
         e = dict(qpos=team_positions(members, P, N, causal), t=t)
         if compute:
             e["q"] = np.concatenate([x[0] for x in qd])
@@ -252,12 +271,25 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
     dkv_part = {}  # rank -> (dK, dV) replica partial for its own team block / or per-unit dict (ext)
     if plan["regime"] == "paper":
         send, recv, nxt, lst = plan["send"], plan["recv"], plan["next"], plan["last"]
-        for r in range(P):
-            t = r // C
-            net.send(1, "INIT_KV", -1, r, send[r], t, 2 * C * n * E * 2, (team[r]["k"], team[r]["v"]) if compute else None)
+        if direct:
+            for r in range(P):
+                b = recv[r] // C
+                for u in range(b * C, b * C + C):
+                    x = loc[u]
+                    net.send(1, "SLICE_KV", -1, u, r, u, 2 * n * E * 2, (x["k"], x["v"]) if compute else None)
+        else:
+            for r in range(P):
+                t = r // C
+                net.send(1, "INIT_KV", -1, r, send[r], t, 2 * C * n * E * 2,
+                         (team[r]["k"], team[r]["v"]) if compute else None)
         stat = {}
         for r in range(P):
-            b, kv = net.recv("INIT_KV", -1, recv[r], r)
+            if direct:
+                b = recv[r] // C
+                kvs = [net.recv("SLICE_KV", -1, u, r)[1] for u in range(b * C, b * C + C)]
+                kv = ((np.concatenate([x[0] for x in kvs]), np.concatenate([x[1] for x in kvs])) if compute else None)
+            else:
+                b, kv = net.recv("INIT_KV", -1, recv[r], r)
             stat[r] = dict(b=b, kv=kv, kpos=team_positions(range(b * C, b * C + C), P, N, causal),
                            dk=np.zeros((C * n, h, d)) if compute else None,
                            dv=np.zeros((C * n, h, d)) if compute else None)

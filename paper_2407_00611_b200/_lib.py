@@ -47,6 +47,9 @@ _SIGS = {
     "wf_plan_trace": (c_int, [c_int, c_int, c_i64, c_int, c_int, c_int, ctypes.POINTER(WfEvent), ctypes.c_size_t,
                               ctypes.POINTER(ctypes.c_size_t)]),
     "wf_plan": (c_int, [c_int, c_int, c_int, c_i32p]),
+    "wf_set_schedule": (c_int, [c_p, c_int]),
+    "wf_plan_trace_sched": (c_int, [c_int, c_int, c_i64, c_int, c_int, c_int, c_int, ctypes.POINTER(WfEvent),
+                                    ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "wf_workspace_bytes": (c_int, [c_int, c_int, c_i64, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_size_t)]),
     "wf_shard_ranges": (c_int, [c_int, c_int, c_i64, c_int, c_i64p]),
     "wf_kernel_launches": (c_i64, [c_p]),

@@ -33,6 +33,7 @@ typedef __nv_bfloat16 bf16;
 struct Geo {
   int P, C, T, R, W;
   bool paper, causal;
+  bool direct;        // DIRECT-PULL init (paper regime): K/V units straight from their owners
   int64_t N;
   int n, c, h, d;     // n rows per rank; c = chunk rows for position tables
   int64_t E;          // h * d
@@ -98,6 +99,7 @@ struct wf_ctx {
   std::string err;
   int debug = 0;
   bool emu_unitpipe = false;  // emulated: run the extension regime unit-pipelined (WF_EMU_UNITPIPE=1)
+  int sched = WF_SCHED_GATHER_SHUFFLE;  // wf_set_schedule
   // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V)
   const void *proj_q = nullptr, *proj_k = nullptr, *proj_v = nullptr;
   int64_t proj_key[4] = {0, 0, 0, 0};
@@ -165,6 +167,7 @@ wf_status check_shape(wf_ctx* ctx, int64_t N, int heads, int head_dim, int causa
   g->R = p.R;
   g->W = p.W;
   g->paper = p.paper;
+  g->direct = ctx->sched == WF_SCHED_DIRECT_PULL && p.paper && p.C > 1;
   g->causal = causal != 0;
   g->N = N;
   g->n = static_cast<int>(N / p.P);
@@ -613,7 +616,11 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   // the K/V slice pull run on the comm stream with one completion event per source rank;
   // the step is cut into (query unit, key unit) launches that merge into the same (O, lse)
   // state, the locally present units first, so the transfers overlap the compute.
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && !g.paper && C > 1;
+  // The K/V units rank r attends first: its slice (extension) or its initial team block
+  // team(recv[r]) (paper regime; pulled unit by unit in the DIRECT-PULL variant).
+  auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
+  const int kcount = g.paper ? C : g.W;
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1));
   if (unitpipe) {
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));
@@ -628,10 +635,9 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         x.fused = pre;
         xs.push_back(x);
       }
-      const int ar = r % C;
-      for (int u = ar * g.W; u < (ar + 1) * g.W; ++u) {
+      for (int u = kfirst(r); u < kfirst(r) + kcount; ++u) {
         if (u == r) continue;
-        const int64_t off = static_cast<int64_t>(u - ar * g.W) * n * E;
+        const int64_t off = static_cast<int64_t>(u - kfirst(r)) * n * E;
         Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
         x.fused = pre;
         x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
@@ -649,8 +655,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
     RankBufs& b = B(ctx, me);
     std::vector<int> qorder, korder;
     for (int i = 0; i < C; ++i) qorder.push_back(t * C + (a + i) % C);  // own unit first
-    for (int i = 0; i < g.W; ++i) {
-      const int u = a * g.W + i;
+    for (int i = 0; i < kcount; ++i) {
+      const int u = kfirst(me) + i;
       if (u == me) korder.insert(korder.begin(), u); else korder.push_back(u);
     }
     for (int qj : qorder) {
@@ -658,7 +664,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       const bf16* qp = qj == me ? Qin(me) : b.qt + jm * n * E;
       for (size_t ki = 0; ki < korder.size(); ++ki) {
         const int u = korder[ki];
-        const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
+        const int64_t koff = static_cast<int64_t>(u - kfirst(me)) * n * E;
         const bf16* kp = u == me ? Kin(me) : b.rk[0] + koff;
         const bf16* vp = u == me ? Vin(me) : b.rv[0] + koff;
         if (ctx->ipc && qj != me) CK(cudaStreamWaitEvent(st, sev[qj], 0));
@@ -698,7 +704,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
           x.segs.push_back({Qin(r), at(lp(p, B(ctx, p).qt), j * n * E), n * E * 2});
           x.fused = pre;
           xs.push_back(x);
-          if (g.paper) {
+          if (g.paper && !g.direct) {
             Xfer y{0, WF_KIND_AG_KV, -1, r, p, r, {}};
             y.fused = pre;
             y.segs.push_back({Kin(r), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
@@ -712,7 +718,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
 
     // Per rank: pointers of the K/V block in ring slot 0/1.
     std::vector<const bf16*> ck0(P, nullptr), cv0(P, nullptr);
-    if (g.paper) {
+    if (g.paper && !g.direct) {
       // Alg. 1 l.2: initial shuffle to init_send (a self "send" keeps the block in place).
       std::vector<Xfer> xs;
       for (int r = 0; r < P; ++r) {
@@ -734,12 +740,12 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         }
       }
     } else {
-      // extension: member a pulls K/V slice a straight from the unit owners.
+      // extension: member a pulls K/V slice a straight from the unit owners (and, in the
+      // DIRECT-PULL variant, every rank its initial team block)
       std::vector<Xfer> xs;
       for (int r = 0; r < P; ++r) {
-        const int a = r % C;
-        for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
-          const int64_t off = static_cast<int64_t>(u - a * g.W) * n * E;
+        for (int u = kfirst(r); u < kfirst(r) + kcount; ++u) {
+          const int64_t off = static_cast<int64_t>(u - kfirst(r)) * n * E;
           Xfer x{0, WF_KIND_SLICE_KV, -1, u, r, u, {}};
           x.fused = pre;
           x.segs.push_back({Kin(u), at(lp(r, B(ctx, r).rk[0]), off), n * E * 2});
@@ -918,7 +924,9 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto pdq = [&](int r, int s) -> float* { return lp(r, B(ctx, r).pdq[s & 1]); };
   std::vector<int> pkg_team(P);
   for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && !g.paper && C > 1;
+  auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
+  const int kcount = g.paper ? C : g.W;
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1));
   if (unitpipe) {
     // Extension regime over peer memory (R = 1): unit-pipelined like the forward.  The
     // gathers of Q, dO, LSE, D and the K/V slice pull run on the comm stream with one
@@ -943,10 +951,9 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
         xs.push_back(y);
       }
-      const int ar = r % C;
-      for (int u = ar * g.W; u < (ar + 1) * g.W; ++u) {
+      for (int u = kfirst(r); u < kfirst(r) + kcount; ++u) {
         if (u == r) continue;
-        const int64_t o = static_cast<int64_t>(u - ar * g.W) * n * E;
+        const int64_t o = static_cast<int64_t>(u - kfirst(r)) * n * E;
         Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
         x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
         x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
@@ -964,8 +971,8 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     CK(cudaMemsetAsync(b.pdq[0], 0, team * 4, st));
     std::vector<int> qorder, korder;
     for (int i = 0; i < C; ++i) qorder.push_back(t * C + (a + i) % C);
-    for (int i = 0; i < g.W; ++i) {
-      const int u = a * g.W + i;
+    for (int i = 0; i < kcount; ++i) {
+      const int u = kfirst(me) + i;
       if (u == me) korder.insert(korder.begin(), u); else korder.push_back(u);
     }
     for (size_t qi = 0; qi < qorder.size(); ++qi) {
@@ -976,7 +983,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       const bf16* dop = own ? L(me, dO, n * E) : b.t_do + jm * n * E;
       for (size_t ki = 0; ki < korder.size(); ++ki) {
         const int u = korder[ki];
-        const int64_t koff = static_cast<int64_t>(u - a * g.W) * n * E;
+        const int64_t koff = static_cast<int64_t>(u - kfirst(me)) * n * E;
         const bf16* kp = u == me ? L(me, K, n * E) : b.rk[0] + koff;
         const bf16* vp = u == me ? L(me, V, n * E) : b.rv[0] + koff;
         if (ctx->ipc && !own) CK(cudaStreamWaitEvent(st, sev[qj], 0));
@@ -1022,7 +1029,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
           y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
           xs.push_back(y);
-          if (g.paper) {
+          if (g.paper && !g.direct) {
             Xfer z{1, WF_KIND_AG_KV, -1, r, p, r, {}};
             z.segs.push_back({L(r, K, n * E), at(lp(p, B(ctx, p).kt), j * n * E), n * E * 2});
             z.segs.push_back({L(r, V, n * E), at(lp(p, B(ctx, p).vt), j * n * E), n * E * 2});
@@ -1038,7 +1045,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     {
       std::vector<Xfer> xs;
       for (int r = 0; r < P; ++r) {
-        if (g.paper) {
+        if (g.paper && !g.direct) {
           const int dst = pl.send[r];
           if (dst == r) continue;
           Xfer x{1, WF_KIND_INIT_KV, -1, r, dst, r / C, {}};
@@ -1046,9 +1053,8 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           x.segs.push_back({vteam(r), lp(dst, B(ctx, dst).rv[0]), team * 2});
           xs.push_back(x);
         } else {
-          const int a = r % C;
-          for (int u = a * g.W; u < (a + 1) * g.W; ++u) {
-            const int64_t o = static_cast<int64_t>(u - a * g.W) * n * E;
+          for (int u = kfirst(r); u < kfirst(r) + kcount; ++u) {
+            const int64_t o = static_cast<int64_t>(u - kfirst(r)) * n * E;
             Xfer x{1, WF_KIND_SLICE_KV, -1, u, r, u, {}};
             x.segs.push_back({L(u, K, n * E), at(lp(r, B(ctx, r).rk[0]), o), n * E * 2});
             x.segs.push_back({L(u, V, n * E), at(lp(r, B(ctx, r).rv[0]), o), n * E * 2});
@@ -1058,7 +1064,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       }
       WCK(run_phase(ctx, xs, tr, st));
       for (int r = 0; r < P; ++r) {
-        const bool self = g.paper && pl.send[r] == r;
+        const bool self = g.paper && !g.direct && pl.send[r] == r;
         sk[r] = self ? kteam(r) : lp(r, B(ctx, r).rk[0]);
         sv[r] = self ? vteam(r) : lp(r, B(ctx, r).rv[0]);
       }
@@ -1389,7 +1395,7 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
   // fused gather: the epilogue writes straight into the team buffers (peer memory or, emulated,
   // the virtual ranks' workspaces); the NCCL transport keeps the separate gather.
   bool fuse = C > 1 && (ctx->emulated || ctx->ipc) && !(ctx->debug & WF_DEBUG_NO_TRANSFER);
-  if (fuse && !g.paper && C + 1 > WF_GEMM_MAX_DST) fuse = false;
+  if (fuse && C + 2 > WF_GEMM_MAX_DST) fuse = false;
   if (fuse && ctx->ipc) WCK(ipc_barrier(ctx, st));  // every peer is done with its team buffers
   auto lp = [&](int r, bf16* p) { return addressable(ctx, r) ? p : nullptr; };
   for (int r = 0; r < P; ++r) {
@@ -1417,15 +1423,17 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
       bool ok = true;
       for (int p = t * C; p < t * C + C; ++p) {  // Alg. 1 l.1: member-major team tensors
         ok = ok && add(0, at(lp(p, B(ctx, p).qt), j * n * E));
-        if (g.paper) {
+        if (g.paper && !g.direct) {
           ok = ok && add(1, at(lp(p, B(ctx, p).kt), j * n * E));
           ok = ok && add(2, at(lp(p, B(ctx, p).vt), j * n * E));
         }
       }
-      if (!g.paper) {  // extension: unit r goes to the ranks whose K/V slice holds it
-        const int a = r / g.W;
-        const int64_t off = static_cast<int64_t>(r - a * g.W) * n * E;
-        for (int p = a; p < P; p += C) {
+      if (!g.paper || g.direct) {  // unit r goes to every rank whose first K/V block holds it
+        for (int p = 0; p < P; ++p) {
+          const int kf = g.paper ? (ctx->plan.recv[p] / C) * C : (p % C) * g.W;
+          const int kc = g.paper ? C : g.W;
+          if (r < kf || r >= kf + kc) continue;
+          const int64_t off = static_cast<int64_t>(r - kf) * n * E;
           ok = ok && add(1, at(lp(p, B(ctx, p).rk[0]), off));
           ok = ok && add(2, at(lp(p, B(ctx, p).rv[0]), off));
         }
@@ -1499,14 +1507,15 @@ wf_status wf_workspace_bytes(int P, int C, int64_t N, int heads, int head_dim, i
   return WF_OK;
 }
 
-wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,
-                        size_t* n_out) {
+wf_status wf_plan_trace_sched(int P, int C, int64_t N, int heads, int head_dim, int rank, int sched, wf_event* buf,
+                              size_t cap, size_t* n_out) {
   wf_ctx* ctx = nullptr;
   wf_ctx* tmp = nullptr;
   WCK(new_ctx(P, C, &ctx, &tmp));
   std::unique_ptr<wf_ctx> hold(ctx);
   ctx->dry = true;
   ctx->dry_rank = rank;
+  ctx->sched = sched;
   Geo g;
   // full-mask geometry (the trace is mask independent)
   wf_status s = check_shape(ctx, N, heads, head_dim, 0, &g);
@@ -1516,6 +1525,20 @@ wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int ra
   if (s == WF_OK) s = backward(ctx, g, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   if (s != WF_OK) return fail(nullptr, s, ctx->err);
   return copy_trace(ctx->trace_fwd, ctx->trace_bwd, buf, cap, n_out);
+}
+
+wf_status wf_plan_trace(int P, int C, int64_t N, int heads, int head_dim, int rank, wf_event* buf, size_t cap,
+                        size_t* n_out) {
+  return wf_plan_trace_sched(P, C, N, heads, head_dim, rank, WF_SCHED_GATHER_SHUFFLE, buf, cap, n_out);
+}
+
+wf_status wf_set_schedule(wf_ctx* ctx, int sched) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  if (sched != WF_SCHED_GATHER_SHUFFLE && sched != WF_SCHED_DIRECT_PULL)
+    return fail(ctx, WF_ERR_CONFIG, "wf_set_schedule: unknown schedule");
+  ctx->sched = sched;
+  ctx->proj_q = ctx->proj_k = ctx->proj_v = nullptr;  // a pending fused gather used the old layout
+  return WF_OK;
 }
 
 wf_status wf_plan(int P, int C, int rank, int32_t out[6]) {

@@ -146,11 +146,14 @@ def _events(buf, n):
     return [(e.pas, KINDS[e.kind], e.step, e.src, e.dst, e.block, e.nbytes) for e in buf[:n]]
 
 
-def plan_trace(P, C, N, heads, head_dim, rank=-1):
+SCHED_GATHER_SHUFFLE, SCHED_DIRECT_PULL = 0, 1
+
+
+def plan_trace(P, C, N, heads, head_dim, rank=-1, sched=SCHED_GATHER_SHUFFLE):
     n = ctypes.c_size_t(0)
-    _check(lib().wf_plan_trace(P, C, N, heads, head_dim, rank, None, 0, ctypes.byref(n)))
+    _check(lib().wf_plan_trace_sched(P, C, N, heads, head_dim, rank, sched, None, 0, ctypes.byref(n)))
     buf = (WfEvent * max(1, n.value))()
-    _check(lib().wf_plan_trace(P, C, N, heads, head_dim, rank, buf, n.value, ctypes.byref(n)))
+    _check(lib().wf_plan_trace_sched(P, C, N, heads, head_dim, rank, sched, buf, n.value, ctypes.byref(n)))
     return _events(buf, n.value)
 
 
@@ -225,6 +228,10 @@ class Context:
         buf = (WfEvent * max(1, n.value))()
         _check(lib().wf_get_trace(self.h, buf, n.value, ctypes.byref(n)), self.h)
         return _events(buf, n.value)
+
+    def set_schedule(self, sched):
+        """SCHED_GATHER_SHUFFLE (the paper's Alg. 1 l.1-2) or SCHED_DIRECT_PULL (wf_set_schedule)."""
+        _check(lib().wf_set_schedule(self.h, int(sched)), self.h)
 
     def set_debug(self, flags):
         """flags: 1 = skip every inter-rank transfer (timing of exposed communication only)."""

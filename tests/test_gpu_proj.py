@@ -79,9 +79,10 @@ def _shards(P, N, causal):
     return np.concatenate([unit_positions(r, P, N, causal) for r in range(P)])
 
 
-@pytest.mark.parametrize("P,C", [(1, 1), (2, 2), (4, 2), (4, 4), (8, 2), (8, 4)])
+@pytest.mark.parametrize("P,C,sched", [(1, 1, 0), (2, 2, 0), (4, 2, 0), (4, 4, 0), (8, 2, 0), (8, 4, 0), (4, 2, 1),
+                                        (8, 2, 1)])
 @pytest.mark.parametrize("causal", [True, False])
-def test_qkv_proj_fused_gather(P, C, causal):
+def test_qkv_proj_fused_gather(P, C, sched, causal):
     wf = _wf()
     h, d, H = 2, 128, 192
     N = 256 * P
@@ -89,6 +90,8 @@ def test_qkv_proj_fused_gather(P, C, causal):
     idx = torch.from_numpy(_shards(P, N, causal))
     xs = x[idx].contiguous().cuda()
     ctx = wf.Context(P, C, emulated=P > 1)
+    if sched:
+        ctx.set_schedule(sched)
     q, k, v = ctx.qkv_proj(xs, w.cuda(), N, h, d, causal)
     o1, l1 = ctx.fwd(q, k, v, N, causal)
     torch.cuda.synchronize()
@@ -101,6 +104,8 @@ def test_qkv_proj_fused_gather(P, C, causal):
         assert ok, worst
     # the fused gather delivers exactly what the separate gather copies
     ctx2 = wf.Context(P, C, emulated=P > 1)
+    if sched:
+        ctx2.set_schedule(sched)
     o2, l2 = ctx2.fwd(q.clone(), k.clone(), v.clone(), N, causal)
     torch.cuda.synchronize()
     tr2 = Counter(e for e in ctx2.trace() if e[0] == 0)

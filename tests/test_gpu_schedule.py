@@ -31,13 +31,15 @@ def shard_index(P, N, causal):
     return np.concatenate([unit_positions(r, P, N, causal) for r in range(P)])
 
 
-def run_path(P, C, N, h, d, causal, seed=0, peaky=True, emulated=True):
+def run_path(P, C, N, h, d, causal, seed=0, peaky=True, emulated=True, sched=0):
     wf = _wf()
     q, k, v, do = make_qkv_do(N, h, d, seed=seed, peaky=peaky)
     idx = torch.from_numpy(shard_index(P, N, causal))
     dev = torch.device("cuda")
     qs, ks, vs, dos = (t[idx].contiguous().to(dev) for t in (q, k, v, do))
     ctx = wf.Context(P, C, emulated=emulated)
+    if sched:
+        ctx.set_schedule(sched)
     o, lse = ctx.fwd(qs, ks, vs, N, causal)
     dq, dk, dv = ctx.bwd(dos, qs, ks, vs, o, lse, N, causal)
     torch.cuda.synchronize()
@@ -60,9 +62,10 @@ def check_values(inputs, outs, causal):
     return ok, errs
 
 
-def oracle_trace(P, C, N, h, d, causal):
-    _, _, ef, _ = simulate_forward(N, None, None, P, C, causal, compute=False, heads=h, head_dim=d)
-    _, _, _, eb = simulate_backward(N, None, None, None, None, None, P, C, causal, compute=False, heads=h, head_dim=d)
+def oracle_trace(P, C, N, h, d, causal, direct=False):
+    _, _, ef, _ = simulate_forward(N, None, None, P, C, causal, compute=False, heads=h, head_dim=d, direct=direct)
+    _, _, _, eb = simulate_backward(N, None, None, None, None, None, P, C, causal, compute=False, heads=h, head_dim=d,
+                                    direct=direct)
     return Counter((e.pas, e.kind, e.step, e.src, e.dst, e.block, e.nbytes) for e in ef + eb)
 
 
@@ -108,3 +111,18 @@ def test_emulated_unit_pipelined_extension(P, C, causal, monkeypatch):
     ok, errs = check_values(inputs, outs, causal)
     assert ok, (P, C, causal, errs)
     assert Counter(trace) == oracle_trace(P, C, N, h, d, causal)
+
+
+@pytest.mark.parametrize("P,C", [(4, 2), (8, 2)])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("unitpipe", ["0", "1"])
+def test_emulated_direct_pull(P, C, causal, unitpipe, monkeypatch):
+    # DIRECT-PULL init (wf_set_schedule, reading c21): values, and the trace of the variant;
+    # at P = 4, C = 2 (R = 1) with WF_EMU_UNITPIPE=1 the unit-pipelined decomposition runs
+    monkeypatch.setenv("WF_EMU_UNITPIPE", unitpipe)
+    N = 256 * P if causal else 128 * P * 2
+    h, d = 2, 128
+    inputs, outs, trace = run_path(P, C, N, h, d, causal, seed=P + C + 5, sched=1)
+    ok, errs = check_values(inputs, outs, causal)
+    assert ok, (P, C, causal, errs)
+    assert Counter(trace) == oracle_trace(P, C, N, h, d, causal, direct=True)

@@ -48,9 +48,10 @@ def test_plan_matches_oracle(wf, P, C):
             (o["send"][r], o["recv"][r], o["next"][r], o["last"][r], o["R"], o["regime"])
 
 
-def _oracle_trace(P, C, N, h, d):
-    _, _, ev_f, _ = simulate_forward(N, None, None, P, C, False, compute=False, heads=h, head_dim=d)
-    _, _, _, ev_b = simulate_backward(N, None, None, None, None, None, P, C, False, compute=False, heads=h, head_dim=d)
+def _oracle_trace(P, C, N, h, d, direct=False):
+    _, _, ev_f, _ = simulate_forward(N, None, None, P, C, False, compute=False, heads=h, head_dim=d, direct=direct)
+    _, _, _, ev_b = simulate_backward(N, None, None, None, None, None, P, C, False, compute=False, heads=h, head_dim=d,
+                                      direct=direct)
     return Counter((e.pas, e.kind, e.step, e.src, e.dst, e.block, e.nbytes) for e in ev_f + ev_b)
 
 
@@ -63,6 +64,14 @@ def test_plan_trace_equals_oracle(wf, P, C):
     N, h, d = 256 * P, 2, 64
     lib_tr = Counter(wf.plan_trace(P, C, N, h, d))
     assert lib_tr == _oracle_trace(P, C, N, h, d)
+
+
+@pytest.mark.parametrize("P,C", CFGS)
+def test_plan_trace_direct_pull_equals_oracle(wf, P, C):
+    # the DIRECT-PULL schedule variant (wf_set_schedule / wf_plan_trace_sched, reading c21)
+    N, h, d = 256 * P, 2, 64
+    lib_tr = Counter(wf.plan_trace(P, C, N, h, d, sched=wf.SCHED_DIRECT_PULL))
+    assert lib_tr == _oracle_trace(P, C, N, h, d, direct=True)
 
 
 def test_plan_trace_per_rank_partition(wf):

@@ -267,3 +267,27 @@ def test_trace_mask_independent_and_deterministic():
     b = simulate_forward(Q, K, V, P, C, True)[2]
     c = simulate_forward(Q, K, V, P, C, True)[2]
     assert a == b == c
+
+
+@pytest.mark.parametrize("P,C", [(4, 2), (8, 2), (16, 4), (16, 2)])
+def test_direct_pull_variant_equals_dense(P, C):
+    # DIRECT-PULL init (reading c21): same values as dense attention and as the default
+    # schedule; no K/V team gather and no init shuffle on the wire, each rank receives the
+    # units of its initial block team(init_recv) from their owners (minus its own unit).
+    N, h, d = 128 * P, 2, 8
+    rng = np.random.default_rng(P * 7 + C)
+    Q, K, V, dO = (rng.standard_normal((N, h, d)) for _ in range(4))
+    for causal in (False, True):
+        O, L, ev_f, _ = simulate_forward(Q, K, V, P, C, causal, direct=True)
+        dq, dk, dv, o, l = attention_bwd(Q, K, V, dO, causal=causal)
+        assert np.abs(O - o).max() < 1e-10 and np.abs(L - l).max() < 1e-10
+        gq, gk, gv, ev_b = simulate_backward(Q, K, V, dO, O, L, P, C, causal, direct=True)
+        assert max(np.abs(gq - dq).max(), np.abs(gk - dk).max(), np.abs(gv - dv).max()) < 1e-10
+    kinds = {e.kind for e in ev_f + ev_b}
+    assert "AG_KV" not in kinds and "INIT_KV" not in kinds
+    plan = build_plan(P, C)
+    for r in range(P):
+        blk = plan["recv"][r] // C
+        want = {u for u in range(blk * C, blk * C + C) if u != r}
+        got = {e.src for e in ev_f if e.kind == "SLICE_KV" and e.dst == r}
+        assert got == want
