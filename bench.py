@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--C", type=int, default=0,
                     help="team size; 0 = the scheduler's grid search (Eq. 8, PAPER.md:302-309) at P > 1")
     ap.add_argument("--seq", type=int, default=0, help="sequence length N (0 = workload default)")
+    ap.add_argument("--sched", default="gather", choices=["gather", "direct"],
+                    help="first K/V block schedule with an explicit --C (paper regime; reading c21)")
     ap.add_argument("--workload", default="gpt", choices=["gpt", "dit"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -189,12 +191,14 @@ def main():
 
     name, N, heads, hd, causal = workload(args, P)
     sched = None
+    schedule = 1 if args.sched == "direct" else 0
     if args.C:
         C = args.C
     elif P > 1:
         from paper_2407_00611_b200 import scheduler
-        C, table = scheduler.search(P, rank, N, heads, hd, causal)
-        sched = {"search": "Eq. 8 argmax over C (PAPER.md:302-309)", "ms_per_step": table, "chosen": C}
+        C, schedule, table = scheduler.search(P, rank, N, heads, hd, causal)
+        sched = {"search": "Eq. 8 argmax over (C, first-block schedule) (PAPER.md:302-309)", "ms_per_step": table,
+                 "chosen": scheduler.label(C, schedule)}
     else:
         C = DEFAULT_C.get(P, 1)
     n = N // P
@@ -202,6 +206,8 @@ def main():
     shape = (n, heads, hd)
     q, k, v, do = (torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16) for _ in range(4))
     ctx = wf.Context(P, C, rank=rank, emulated=False)
+    if schedule:
+        ctx.set_schedule(schedule)
     o = torch.empty_like(q)
     lse = torch.empty((heads, n), dtype=torch.float32, device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
@@ -360,7 +366,7 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) bf16, resident in HBM",
             "config": {"workload": name, "N": N, "heads": heads, "head_dim": hd, "causal": causal, "P": P, "C": C,
-                       "parallelism": f"sp{P} (WallFacer teams of {C})",
+                       "parallelism": f"sp{P} (WallFacer teams of {C}" + (", direct-pull init)" if schedule else ")"),
                        "l2": "inputs (4 x N/P x h x d bf16) exceed L2 (126 MB) per step" if q.numel() * 8 > 126e6 else "inputs fit L2"},
             "tflops_per_gpu": total_tflops / world,
             "frac_of_peak_per_gpu": total_tflops / world / peak,

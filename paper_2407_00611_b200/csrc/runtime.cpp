@@ -100,6 +100,9 @@ struct wf_ctx {
   int debug = 0;
   bool emu_unitpipe = false;  // emulated: run the extension regime unit-pipelined (WF_EMU_UNITPIPE=1)
   int sched = WF_SCHED_GATHER_SHUFFLE;  // wf_set_schedule
+  // DIRECT-PULL at R = 1 unit-pipelined (WF_DIRECT_UNITPIPE=1): measured slower at P = 4,
+  // C = 2 than one whole-block launch after the pulls (small launches), so off by default
+  bool direct_unitpipe = false;
   // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V)
   const void *proj_q = nullptr, *proj_k = nullptr, *proj_v = nullptr;
   int64_t proj_key[4] = {0, 0, 0, 0};
@@ -620,7 +623,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   // team(recv[r]) (paper regime; pulled unit by unit in the DIRECT-PULL variant).
   auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
   const int kcount = g.paper ? C : g.W;
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1));
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1 && ctx->direct_unitpipe));
   if (unitpipe) {
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));
@@ -926,7 +929,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
   auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
   const int kcount = g.paper ? C : g.W;
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1));
+  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1 && ctx->direct_unitpipe));
   if (unitpipe) {
     // Extension regime over peer memory (R = 1): unit-pipelined like the forward.  The
     // gathers of Q, dO, LSE, D and the K/V slice pull run on the comm stream with one
@@ -1333,6 +1336,8 @@ wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, w
     // transport: peer-memory copies + flags (default) or NCCL send/recv (WF_TRANSPORT=nccl)
     const char* tp = std::getenv("WF_TRANSPORT");
     ctx->ipc = !(tp && std::string(tp) == "nccl") && P <= kMaxRanks;
+    const char* du = std::getenv("WF_DIRECT_UNITPIPE");
+    ctx->direct_unitpipe = du && du[0] == '1';
   }
   *out = ctx;
   return WF_OK;
@@ -1346,6 +1351,8 @@ wf_status wf_init_emulated(int P, int C, wf_ctx** out) {
   ctx->emulated = true;
   const char* up = std::getenv("WF_EMU_UNITPIPE");
   ctx->emu_unitpipe = up && up[0] == '1';
+  const char* du = std::getenv("WF_DIRECT_UNITPIPE");
+  ctx->direct_unitpipe = du && du[0] == '1';
   wf_status s = make_streams(ctx);
   if (s != WF_OK) {
     g_ctxless_err = ctx->err;

@@ -120,6 +120,7 @@ def test_emulated_direct_pull(P, C, causal, unitpipe, monkeypatch):
     # DIRECT-PULL init (wf_set_schedule, reading c21): values, and the trace of the variant;
     # at P = 4, C = 2 (R = 1) with WF_EMU_UNITPIPE=1 the unit-pipelined decomposition runs
     monkeypatch.setenv("WF_EMU_UNITPIPE", unitpipe)
+    monkeypatch.setenv("WF_DIRECT_UNITPIPE", unitpipe)
     N = 256 * P if causal else 128 * P * 2
     h, d = 2, 128
     inputs, outs, trace = run_path(P, C, N, h, d, causal, seed=P + C + 5, sched=1)

@@ -23,6 +23,9 @@ for C in [int(c) for c in os.environ.get("CS", "1 2 4").split()]:
         idx = torch.from_numpy(unit_positions(rank, world, N, causal))
         qs, ks, vs, dos = (t[idx].contiguous().cuda() for t in (qg, kg, vg, dog))
         ctx = wf.Context(world, C, rank=rank)
+        direct = os.environ.get("SCHED") == "direct" and C > 1 and C * C <= world
+        if direct:
+            ctx.set_schedule(wf.SCHED_DIRECT_PULL)
         o, lse = ctx.fwd(qs, ks, vs, N, causal)
         dq, dk, dv = ctx.bwd(dos, qs, ks, vs, o, lse, N, causal)
         torch.cuda.synchronize()
@@ -42,8 +45,10 @@ for C in [int(c) for c in os.environ.get("CS", "1 2 4").split()]:
                     [np.abs(g - ref[pos]).max() / np.abs(ref).max() for g, ref in ((dq_, dq_r), (dk_, dk_r), (dv_, dv_r))]
                 line.append("r%d " % r + " ".join("%.3g" % x for x in e))
                 trace += t
-            _, _, ef, _ = simulate_forward(N, None, None, world, C, causal, compute=False, heads=h, head_dim=d)
-            _, _, _, eb = simulate_backward(N, None, None, None, None, None, world, C, causal, compute=False, heads=h, head_dim=d)
+            _, _, ef, _ = simulate_forward(N, None, None, world, C, causal, compute=False, heads=h, head_dim=d,
+                                           direct=direct)
+            _, _, _, eb = simulate_backward(N, None, None, None, None, None, world, C, causal, compute=False, heads=h,
+                                            head_dim=d, direct=direct)
             ref = Counter((e.pas, e.kind, e.step, e.src, e.dst, e.block, e.nbytes) for e in ef + eb)
             got = Counter(trace)
             print(f"C={C} causal={causal} trace_ok={got == ref}", " | ".join(line), flush=True)
