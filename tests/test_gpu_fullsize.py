@@ -154,3 +154,37 @@ def test_max_length_sampled(N):
     s_dv = dv.float().sum(0)
     s_do = do.float().sum(0)
     assert (s_dv - s_do).abs().max().item() <= 2e-3 * do.float().abs().sum(0).max().item()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("C", [4, 2])
+def test_target_config_emulated_p8(C, monkeypatch):
+    # BASELINE's target: GPT 32 x 128 causal, N = 128K, P = 8 (C = 4: extension regime with
+    # the real-mode unit-pipelined decomposition, two key units per slice; C = 2: paper regime,
+    # R = 2 ring), all eight ranks emulated on one GPU: sampled rows of two heads against the
+    # oracle, and the dV column-sum identity over the whole sequence
+    monkeypatch.setenv("WF_EMU_UNITPIPE", "1")
+    wf = _wf()
+    from oracle.sharding import unit_positions
+    P, N, h, d = 8, 131072, 32, 128
+    g = torch.Generator(device="cuda").manual_seed(21)
+    q, k, v, do = (torch.randn((N, h, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    idx = torch.from_numpy(np.concatenate([unit_positions(r, P, N, True) for r in range(P)])).cuda()
+    qs, ks, vs, dos = (t[idx].contiguous() for t in (q, k, v, do))
+    ctx = wf.Context(P, C, emulated=True)
+    o, lse = ctx.fwd(qs, ks, vs, N, True)
+    dq, dk, dv = ctx.bwd(dos, qs, ks, vs, o, lse, N, True)
+    torch.cuda.synchronize()
+    ctx.close()
+    inv = torch.argsort(idx)
+    o_g = o[inv]
+    lse_g = lse.reshape(P, h, N // P).permute(1, 0, 2).reshape(h, N)[:, inv]
+    rows = np.array([0, 4097, N // 2 - 1, N // 2 + 3, N - 1])
+    for hh in (0, h - 1):
+        K, V = to_f64(k[:, hh:hh + 1].cpu()), to_f64(v[:, hh:hh + 1].cpu())
+        Q = to_f64(q[rows, hh:hh + 1].cpu())
+        o_ref, l_ref = attention_fwd(Q, K, V, qpos=rows, kpos=np.arange(N), causal=True)
+        assert np.abs(to_f64(o_g[rows, hh:hh + 1].cpu()) - o_ref).max() <= 2e-2
+        assert np.abs(lse_g[hh, rows].double().cpu().numpy() - l_ref[0]).max() <= 1e-2
+    s_dv, s_do = dv.float().sum(0), do.float().sum(0)
+    assert (s_dv - s_do).abs().max().item() <= 2e-3 * do.float().abs().sum(0).max().item()
