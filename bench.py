@@ -288,7 +288,7 @@ def main():
     # pipeline), and the timed region spans the first upload to the last download.
     e2e = None
     if not args.no_e2e:
-        steps_e = max(3, min(args.steps, 6))
+        steps_e = max(3, args.steps)
         hin = [[x.cpu().pin_memory() for x in (q, k, v, do)] for _ in range(2)]
         hout = [[torch.empty_like(hin[0][0]).pin_memory() for _ in range(4)] +
                 [torch.empty((heads, n), dtype=torch.float32).pin_memory()] for _ in range(2)]
