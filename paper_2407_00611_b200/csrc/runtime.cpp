@@ -360,16 +360,23 @@ cudaEvent_t pool_event(wf_ctx* ctx);
 cudaEvent_t prof_begin(wf_ctx* ctx, cudaStream_t st);
 
 // ------------------------------------------------------------------ transport
-wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& trace, cudaStream_t st) {
-  for (const Xfer& x : xs) {
-    if (x.src == x.dst || !recorded(ctx, x.src)) continue;
-    int64_t bytes = 0;
-    for (const Seg& s : x.segs) bytes += s.bytes;
-    trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
+// part: kPhaseAll, or (peer-memory transport) kPhaseSend = trace + copies + signals only and
+// kPhaseWait = the matching waits only, so a sender can release a slot between the two.
+enum { kPhaseAll = 0, kPhaseSend = 1, kPhaseWait = 2 };
+wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& trace, cudaStream_t st,
+                    int part = kPhaseAll) {
+  if (part != kPhaseWait) {
+    for (const Xfer& x : xs) {
+      if (x.src == x.dst || !recorded(ctx, x.src)) continue;
+      int64_t bytes = 0;
+      for (const Seg& s : x.segs) bytes += s.bytes;
+      trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
+    }
   }
   if (ctx->dry) return WF_OK;
   if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
   if (ctx->emulated) {
+    if (part == kPhaseWait) return WF_OK;
     for (const Xfer& x : xs)
       if (!x.fused)
         for (const Seg& s : x.segs)
@@ -380,20 +387,22 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
   if (ctx->ipc) {
     const int ch = st == ctx->comm_stream ? 1 : 0;
     cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
-    for (const Xfer& x : xs) {
-      if (x.src != me || x.pull || x.fused) continue;
-      for (const Seg& sg : x.segs)
-        if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
+    if (part != kPhaseWait) {
+      for (const Xfer& x : xs) {
+        if (x.src != me || x.pull || x.fused) continue;
+        for (const Seg& sg : x.segs)
+          if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
+      }
     }
     SigArgs sig{}, wt{};
     bool dst_done[kMaxRanks] = {}, src_done[kMaxRanks] = {};
     for (const Xfer& x : xs) {
-      if (x.src == me && x.dst != me && !dst_done[x.dst]) {
+      if (part != kPhaseWait && x.src == me && x.dst != me && !dst_done[x.dst]) {
         dst_done[x.dst] = true;
         sig.dst[sig.n] = flag_of(ctx, x.dst, ch * 64 + me);
         sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
       }
-      if (x.dst == me && x.src != me && !src_done[x.src]) {
+      if (part != kPhaseSend && x.dst == me && x.src != me && !src_done[x.src]) {
         src_done[x.src] = true;
         wt.dst[wt.n] = flag_of(ctx, me, ch * 64 + x.src);
         wt.val[wt.n++] = ++ctx->rcvd[ch][x.src];
@@ -818,8 +827,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
           // slot as soon as next has released it (its step s-1), independent of my compute.
           if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
-          WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
-          CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
+          WCK(run_phase(ctx, xs, tr, ctx->comm_stream, kPhaseSend));
         } else if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
           CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
@@ -830,7 +838,14 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (local(ctx, r)) WCK(compute(r, s));
       if (s < R - 1) {
         if (overlap && ctx->ipc) {
-          WCK(ipc_ack(ctx, pl.last[ctx->rank], st));  // my slot s is free again
+          // my slot s is free again once my kernel has read it AND my comm stream has
+          // forwarded it to next (the send above): release it from the comm stream after
+          // both, then wait for block s+1 from last
+          CK(cudaEventRecord(ctx->ev_b, st));
+          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+          WCK(ipc_ack(ctx, pl.last[ctx->rank], ctx->comm_stream));
+          WCK(run_phase(ctx, xs, tr, ctx->comm_stream, kPhaseWait));
+          CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
           CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
         } else if (overlap) {
           CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
@@ -1098,7 +1113,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           // the package does not depend on step s: push it as soon as next released the slot
           if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
-          WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
+          WCK(run_phase(ctx, pk, tr, ctx->comm_stream, kPhaseSend));
         } else if (overlap) {  // the package does not depend on step s: post it first
           CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
@@ -1138,12 +1153,16 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       }
       if (s < R - 1) {
         if (overlap && ctx->ipc) {
-          // dQ depends on step s: push it after the step, then release my slot
+          // dQ depends on step s: push it after the step; my package and dQ slots are free
+          // once my kernel has read them and both sends have left (comm stream order), so
+          // the release goes out from the comm stream after them; then wait for step s+1
           CK(cudaEventRecord(ctx->ev_b, st));
           CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
-          WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
+          WCK(run_phase(ctx, dq, tr, ctx->comm_stream, kPhaseSend));
+          WCK(ipc_ack(ctx, pl.last[ctx->rank], ctx->comm_stream));
+          WCK(run_phase(ctx, pk, tr, ctx->comm_stream, kPhaseWait));
+          WCK(run_phase(ctx, dq, tr, ctx->comm_stream, kPhaseWait));
           CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
-          WCK(ipc_ack(ctx, pl.last[ctx->rank], st));
           CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
         } else if (overlap) {
           // dQ depends on step s: after it; the receiver's next step waits for both

@@ -1,0 +1,62 @@
+"""GPU-box: locate non-reproducible forward outputs in the real multi-rank path (torchrun).
+For C = CSTRESS (default 1) and each shape, run ITERS fwd(+bwd) calls and report the
+iterations whose O differs from iteration 0, with the max abs difference."""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2407_00611_b200 as wf  # noqa: E402
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+C = int(os.environ.get("CSTRESS", "1"))
+iters = int(os.environ.get("ITERS", "20"))
+bwd = os.environ.get("BWD", "1") == "1"
+sync_each = os.environ.get("SYNC", "0") == "1"
+h, d = 8, 128
+shapes = [int(x) * world for x in os.environ.get("NS", "2048").split(",")]
+ctx = wf.Context(world, C, rank=rank)
+for N in shapes:
+    for causal in (True, False):
+        n = N // world
+        g = torch.Generator(device="cuda").manual_seed(rank * 7 + N)
+        q, k, v, do = (torch.randn((n, h, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+        outs = []
+        for it in range(iters):
+            o, lse = ctx.fwd(q, k, v, N, causal)
+            if bwd:
+                ctx.bwd(do, q, k, v, o, lse, N, causal)
+            outs.append(o.clone())
+            if sync_each:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        bad = [(i, float((x.float() - outs[0].float()).abs().max())) for i, x in enumerate(outs) if not torch.equal(x, outs[0])]
+        # reference for my rows: one block kernel over the gathered global K/V with positions
+        from oracle.sharding import unit_positions
+        ks_all = [torch.empty_like(k) for _ in range(world)]
+        vs_all = [torch.empty_like(v) for _ in range(world)]
+        dist.all_gather(ks_all, k)
+        dist.all_gather(vs_all, v)
+        if causal:
+            pos = [unit_positions(r, world, N, True) for r in range(world)]
+            half = n // 2
+            qstart = [int(pos[rank][0]), int(pos[rank][half])]
+            kstart = [int(x) for r in range(world) for x in (pos[r][0], pos[r][half])]
+            _, ob, _ = wf.block_fwd(q, torch.cat(ks_all), torch.cat(vs_all), causal=True, chunk=half, qstart=qstart,
+                                    kstart=kstart)
+        else:
+            _, ob, _ = wf.block_fwd(q, torch.cat(ks_all), torch.cat(vs_all), causal=False)
+        torch.cuda.synchronize()
+        ref_err = [float((outs[i].float() - ob.float()).abs().max()) for i in (0, 1, iters - 1)]
+        bad.append(("ref_err(it0,it1,last)", ref_err))
+        allb = [None] * world
+        dist.all_gather_object(allb, bad[:6])
+        if rank == 0:
+            print(f"C={C} N={N} causal={causal} bwd={bwd} sync={sync_each}: " +
+                  " | ".join(f"r{r}:{b}" for r, b in enumerate(allb)), flush=True)
+ctx.close()
+dist.destroy_process_group()
