@@ -25,11 +25,12 @@ for N in shapes:
         n = N // world
         g = torch.Generator(device="cuda").manual_seed(rank * 7 + N)
         q, k, v, do = (torch.randn((n, h, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
-        outs = []
+        outs, grads = [], []
         for it in range(iters):
             o, lse = ctx.fwd(q, k, v, N, causal)
             if bwd:
-                ctx.bwd(do, q, k, v, o, lse, N, causal)
+                dq, dk, dv = ctx.bwd(do, q, k, v, o, lse, N, causal)
+                grads.append(torch.cat([dq.float().flatten(), dk.float().flatten(), dv.float().flatten()]))
             outs.append(o.clone())
             if sync_each:
                 torch.cuda.synchronize()
@@ -53,6 +54,10 @@ for N in shapes:
         torch.cuda.synchronize()
         ref_err = [float((outs[i].float() - ob.float()).abs().max()) for i in (0, 1, iters - 1)]
         bad.append(("ref_err(it0,it1,last)", ref_err))
+        if grads:  # gradients are reproducible up to the fp32 dQ reduction order
+            gmax = float(grads[0].abs().max())
+            gdev = max(float((x - grads[0]).abs().max()) for x in grads) / gmax
+            bad.append(("grad_dev", round(gdev, 6)))
         allb = [None] * world
         dist.all_gather_object(allb, bad[:6])
         if rank == 0:
