@@ -182,7 +182,9 @@ wf_status wf_debug_timeline_read(unsigned long long* out, size_t n);
 /* Last error text of ctx (or of the last context-less call when ctx is NULL). */
 const char* wf_last_error(const wf_ctx* ctx);
 
-/* Destroy the context: frees workspace, communicators, streams. */
+/* Destroy the context: frees workspace, communicators, streams.  Collective over the P
+ * ranks of a real (peer-memory) context: the workspace is freed only after every rank has
+ * finished its last call, since peers read it in place. */
 wf_status wf_finalize(wf_ctx* ctx);
 
 /* ---- per-step kernels, exported for parity tests of one ring step ---------------

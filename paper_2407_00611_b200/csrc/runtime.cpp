@@ -260,6 +260,8 @@ uint32_t* flag_of(wf_ctx* ctx, int owner, int word) {
   return reinterpret_cast<uint32_t*>(ctx->peer_base[owner]) + word;
 }
 
+wf_status ipc_barrier(wf_ctx* ctx, cudaStream_t st);
+
 // ------------------------------------------------------------------ workspace
 // the workspace carve of one rank (bytes per buffer, in carve order)
 using CarveList = std::vector<std::pair<void**, int64_t>>;
@@ -321,6 +323,12 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   if (ctx->ws && std::equal(key, key + 4, ctx->ws_key)) return WF_OK;
   if (ctx->ws) {
     CK(cudaDeviceSynchronize());
+    if (ctx->ipc) {
+      // peers may still be reading (pull kernels) or signalling into this workspace from
+      // their previous call: free it only after every rank has finished that call
+      WCK(ipc_barrier(ctx, ctx->comm_stream));
+      CK(cudaStreamSynchronize(ctx->comm_stream));
+    }
     for (size_t r = 0; r < ctx->peer_base.size(); ++r)
       if (static_cast<int>(r) != ctx->rank && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
     ctx->peer_base.clear();
@@ -1659,6 +1667,11 @@ wf_status wf_finalize(wf_ctx* ctx) {
   if (!ctx) return WF_OK;
   if (ctx->ws) {
     cudaDeviceSynchronize();
+    if (ctx->ipc && ctx->comm_stream && !ctx->peer_base.empty()) {
+      // collective: peers may still pull from this workspace -- free it after every rank
+      // has finished its last call (a rank that never joins makes the wait trap in 30 s)
+      if (ipc_barrier(ctx, ctx->comm_stream) == WF_OK) cudaStreamSynchronize(ctx->comm_stream);
+    }
     for (size_t r = 0; r < ctx->peer_base.size(); ++r)
       if (static_cast<int>(r) != ctx->rank && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
     cudaFree(ctx->ws);
