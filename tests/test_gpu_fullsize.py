@@ -188,3 +188,30 @@ def test_target_config_emulated_p8(C, monkeypatch):
         assert np.abs(lse_g[hh, rows].double().cpu().numpy() - l_ref[0]).max() <= 1e-2
     s_dv, s_do = dv.float().sum(0), do.float().sum(0)
     assert (s_dv - s_do).abs().max().item() <= 2e-3 * do.float().abs().sum(0).max().item()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("C", [1, 2, 4])
+def test_dit_config_emulated_p8(C, monkeypatch):
+    # BASELINE's DiT config: 16 heads x 72, full mask, N = 64K, P = 8, every C; all ranks
+    # emulated on one GPU (C = 4 unit-pipelined): sampled rows of two heads, dV identity
+    monkeypatch.setenv("WF_EMU_UNITPIPE", "1")
+    wf = _wf()
+    P, N, h, d = 8, 65536, 16, 72
+    g = torch.Generator(device="cuda").manual_seed(31 + C)
+    q, k, v, do = (torch.randn((N, h, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    ctx = wf.Context(P, C, emulated=True)
+    o, lse = ctx.fwd(q, k, v, N, False)        # full mask: contiguous shards, rank-major = global order
+    dq, dk, dv = ctx.bwd(do, q, k, v, o, lse, N, False)
+    torch.cuda.synchronize()
+    ctx.close()
+    lse_g = lse.reshape(P, h, N // P).permute(1, 0, 2).reshape(h, N)
+    rows = np.array([0, 999, N // 2, N - 1])
+    for hh in (0, h - 1):
+        K, V = to_f64(k[:, hh:hh + 1].cpu()), to_f64(v[:, hh:hh + 1].cpu())
+        Q = to_f64(q[rows, hh:hh + 1].cpu())
+        o_ref, l_ref = attention_fwd(Q, K, V, qpos=rows, kpos=np.arange(N), causal=False)
+        assert np.abs(to_f64(o[rows, hh:hh + 1].cpu()) - o_ref).max() <= 2e-2
+        assert np.abs(lse_g[hh, rows].double().cpu().numpy() - l_ref[0]).max() <= 1e-2
+    s_dv, s_do = dv.float().sum(0), do.float().sum(0)
+    assert (s_dv - s_do).abs().max().item() <= 2e-3 * do.float().abs().sum(0).max().item()
