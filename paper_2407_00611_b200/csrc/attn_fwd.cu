@@ -411,6 +411,7 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s) {
   if (a.nq <= 0 || a.nq % WF_TILE || a.nk % WF_TILE) return cudaErrorInvalidValue;
+  if (block_fwd_split_ok(a, D)) return launch_block_fwd_split(tq, tk, tv, a, s);
   if (a.kbase && a.nk > 0 && block_fwd_pair_ok(a, D)) {
     CUtensorMap tk64;
     if (make_tmap_rows_box(&tk64, a.kbase, a.nk, a.heads, D, 64)) {

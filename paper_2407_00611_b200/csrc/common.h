@@ -171,6 +171,10 @@ cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
+// split-row forward (attn_fwd3.cu): head_dim 128, two softmax threads per row (WF_FWD_SPLIT=1)
+bool block_fwd_split_ok(const FwdArgs& a, int D);
+cudaError_t launch_block_fwd_split(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                   const FwdArgs& a, cudaStream_t s);
 // CTA-pair forward (attn_fwd2.cu): head_dim 128, nq % 512 == 0, opt-in with WF_FWD_PAIR=1
 bool block_fwd_pair_ok(const FwdArgs& a, int D);
 cudaError_t launch_block_fwd_pair(const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,

@@ -164,3 +164,18 @@ def test_block_fwd_cta_pair(causal, case, monkeypatch):
         o, l = to_f64(ob), lse.cpu().double().numpy()
     eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
     assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("case", ["contiguous", "zigzag"])
+def test_block_fwd_split_rows(causal, case, monkeypatch):
+    """The opt-in split-row forward (attn_fwd3.cu, WF_FWD_SPLIT=1): two softmax threads per
+    query row, partial maxima exchanged through shared memory."""
+    monkeypatch.setenv("WF_FWD_SPLIT", "1")
+    if case == "contiguous":
+        o, l, o_ref, l_ref = _run_fwd(1024, 1024, 2, 128, causal, 1024, [0], [0], peaky=True)
+    else:
+        o, l, o_ref, l_ref = _run_fwd(1024, 1024, 3, 128, causal, 256, [0, 1792, 512, 1280], [256, 1536, 768, 1024],
+                                      peaky=True)
+    eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
