@@ -606,6 +606,36 @@ wf_status join_comm(wf_ctx* ctx, cudaStream_t st) {
   return WF_OK;
 }
 
+// Unit-pipelined passes run the query units of member a in the order a, a+1, ..., a+C-1
+// (team-relative): member i's last unit is that of member i-1.
+bool last_unit_of(int C, int i, int j) { return (j + 1) % C == i; }
+
+// push a finished partial into its owner's slot: a copy-engine copy on the comm stream after
+// the producing kernel (peer memory), or a device copy in stream order (emulated)
+wf_status push_segs(wf_ctx* ctx, const Seg* segs, int nseg, cudaStream_t st) {
+  if (ctx->ipc) {
+    CK(cudaEventRecord(ctx->ev_b, st));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+  }
+  for (int i = 0; i < nseg; ++i)
+    CK(cudaMemcpyAsync(segs[i].dst, segs[i].src, segs[i].bytes, cudaMemcpyDefault, ctx->ipc ? ctx->comm_stream : st));
+  return WF_OK;
+}
+
+// a reduce-scatter phase whose senders pushed part of it from the comm stream: the signals
+// go out from the comm stream after those pushes and after my compute, the caller's stream
+// waits for the matching arrivals
+wf_status run_phase_after_pushes(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& tr, cudaStream_t st,
+                                 bool pushed) {
+  if (!pushed || !ctx->ipc) return run_phase(ctx, xs, tr, st);
+  CK(cudaEventRecord(ctx->ev_b, st));
+  CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
+  WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
+  CK(cudaEventRecord(ctx->ev_c, ctx->comm_stream));
+  CK(cudaStreamWaitEvent(st, ctx->ev_c, 0));
+  return WF_OK;
+}
+
 // ------------------------------------------------------------------ forward
 wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const bf16* V, bf16* O, float* LSE,
                   cudaStream_t st) {
@@ -679,7 +709,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       const int u = kfirst(me) + i;
       if (u == me) korder.insert(korder.begin(), u); else korder.push_back(u);
     }
-    for (int qj : qorder) {
+    for (size_t qi = 0; qi < qorder.size(); ++qi) {
+      const int qj = qorder[qi];
       const int jm = qj - t * C;
       const bf16* qp = qj == me ? Qin(me) : b.qt + jm * n * E;
       for (size_t ki = 0; ki < korder.size(); ++ki) {
@@ -710,6 +741,13 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         cudaEvent_t e0 = prof_begin(ctx, st);
         WCK(kcheck(ctx, launch_block_fwd(tq, tk, tv, fa, g.d, st), "block_fwd"));
         prof_end(ctx, st, e0, ctx->ev_fwd);
+      }
+      // member qj's partial is final; unless it is my last unit (which its owner reads in
+      // place), push it into qj's merge slot while the next units run
+      if (qj != me && qi + 1 < qorder.size() && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) {
+        const Seg segs[2] = {{b.o_state + jm * n * E, B(ctx, qj).rs_o + a * n * E, n * E * 4},
+                             {b.lse_state + jm * h * n, B(ctx, qj).rs_lse + a * h * n, h * n * 4}};
+        WCK(push_segs(ctx, segs, 2, st));
       }
     }
     }  // ranks
@@ -877,15 +915,17 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         const int jp = p - t * C;
         // peer-memory transport: the owner's merge kernel reads the partial in place
         // (fused reduce-scatter); otherwise it is copied into the owner's slot first.
-        Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}, ctx->ipc};
+        // Unit-pipelined: all but the sender's last unit were pushed already (above).
+        const bool pushed = unitpipe && !last_unit_of(C, j, jp);
+        Xfer x{0, WF_KIND_RS_O, R, r, p, p, {}, ctx->ipc && !pushed, pushed};
         x.segs.push_back({at(lp(r, B(ctx, r).o_state), jp * n * E), at(lp(p, B(ctx, p).rs_o), j * n * E), n * E * 4});
         xs.push_back(x);
-        Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}, ctx->ipc};
+        Xfer y{0, WF_KIND_RS_LSE, R, r, p, p, {}, ctx->ipc && !pushed, pushed};
         y.segs.push_back({at(lp(r, B(ctx, r).lse_state), jp * h * n), at(lp(p, B(ctx, p).rs_lse), j * h * n), h * n * 4});
         xs.push_back(y);
       }
     }
-    WCK(run_phase(ctx, xs, tr, st));
+    WCK(run_phase_after_pushes(ctx, xs, tr, st, unitpipe));
     for (int r = 0; r < P; ++r) {
       if (!local(ctx, r)) continue;
       RankBufs& b = B(ctx, r);
@@ -900,7 +940,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (i == j) {
           m.o[i] = b.o_state + i * n * E;
           m.lse[i] = b.lse_state + i * h * n;
-        } else if (ctx->ipc) {  // member i's partial of my rows, read over NVLink
+        } else if (ctx->ipc && (!unitpipe || last_unit_of(C, i, j))) {  // read in place over NVLink
           m.o[i] = B(ctx, t0 + i).o_state + j * n * E;
           m.lse[i] = B(ctx, t0 + i).lse_state + j * h * n;
         } else {
@@ -1037,6 +1077,11 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         cudaEvent_t e0 = prof_begin(ctx, st);
         WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, ba, g.d, st), "block_bwd"));
         prof_end(ctx, st, e0, ctx->ev_bwd);
+      }
+      // member qj's dQ partial is final: pushed like the forward partials
+      if (!own && qi + 1 < qorder.size() && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) {
+        const Seg sg{b.pdq[0] + jm * n * E, B(ctx, qj).rsq + a * n * E, n * E * 4};
+        WCK(push_segs(ctx, &sg, 1, st));
       }
     }
     }  // ranks
@@ -1260,19 +1305,22 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       for (int p = t * C; p < t * C + C; ++p) {
         if (p == r) continue;
         const int jp = p - t * C;
-        Xfer x{1, WF_KIND_RS_DQ, R, r, p, p, {}, ctx->ipc};
+        const bool pushed = unitpipe && !last_unit_of(C, j, jp);
+        Xfer x{1, WF_KIND_RS_DQ, R, r, p, p, {}, ctx->ipc && !pushed, pushed};
         x.segs.push_back({at(home[r], jp * n * E), at(lp(p, B(ctx, p).rsq), j * n * E), n * E * 4});
         xs.push_back(x);
       }
     }
-    WCK(run_phase(ctx, xs, tr, st));
+    WCK(run_phase_after_pushes(ctx, xs, tr, st, unitpipe));
   }
   for (int r = 0; r < P; ++r) {
     const int j = r % C;
     for (int i = 0; i < C; ++i) {
       const int ri = (r / C) * C + i;
-      qparts[r].push_back(i == j ? at(home[r], i * n * E)
-                                 : ctx->ipc ? at(home[ri], j * n * E) : at(lp(r, B(ctx, r).rsq), i * n * E));
+      const bool in_place = ctx->ipc && (!unitpipe || last_unit_of(C, i, j));
+      qparts[r].push_back(i == j     ? at(home[r], i * n * E)
+                          : in_place ? at(home[ri], j * n * E)
+                                     : at(lp(r, B(ctx, r).rsq), i * n * E));
     }
   }
   if (ctx->dry) return WF_OK;
