@@ -109,6 +109,11 @@ def predict(P, C, N, heads, head_dim, causal, fwd_tflops, bwd_tflops, link_gbps=
     res = {"P": P, "C": C, "R": R, "regime": "ext" if ext else "paper"}
     for pas, comp, hop in ((0, comp_f, step_f), (1, comp_b, step_b)):
         pre, post = phase_ms(pas, _PRE), phase_ms(pas, _POST)
+        if ext and C > 1:
+            # unit-pipelined: of the C-1 member partials a rank receives, all but the one its
+            # sender finishes last were pushed during later units; only that one is exposed
+            rs = {"RS_O", "RS_LSE", "RS_DQ"}
+            post = phase_ms(pas, _POST - rs) + phase_ms(pas, rs) / (C - 1)
         if R > 1:
             per = comp / R
             ring = per + (R - 1) * max(per, hop / (link_gbps * 1e9) * 1e3 + lat)
