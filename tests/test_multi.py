@@ -110,7 +110,7 @@ def _gpu_worker(rank, world, port, C, N, causal, q):
 
 @pytest.mark.gpu
 @pytest.mark.multigpu
-@pytest.mark.parametrize("C", [1, 2])
+@pytest.mark.parametrize("C", [1, 2, 4])
 @pytest.mark.parametrize("causal", [True, False])
 def test_nccl_real_path(C, causal):
     from oracle.dense import attention_bwd
@@ -144,6 +144,37 @@ def test_nccl_real_path(C, causal):
         assert all(e[3] == r for e in tr)
         trace += tr
     assert Counter(trace) == Counter(_oracle_events(world, C, N, h, d, causal))
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+def test_real_path_multi_tile_units():
+    """C = GPU count (unit-pipelined, partial pushes) with units of 16 query tiles per rank."""
+    from oracle.dense import attention_bwd
+    from oracle.sharding import unit_positions
+    from wf_inputs import make_qkv_do, to_f64
+    world = min(torch.cuda.device_count(), 4)
+    C, N, causal = world, 2048 * world, True
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, C, N, causal, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allres = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    h, d = 2, 128
+    qg, kg, vg, dog = make_qkv_do(N, h, d, seed=21, peaky=True)
+    dq_r, dk_r, dv_r, o_r, l_r = attention_bwd(to_f64(qg), to_f64(kg), to_f64(vg), to_f64(dog), causal=causal)
+    for r, (res, _) in enumerate(allres):
+        pos = unit_positions(r, world, N, causal)
+        o, lse, dq, dk, dv = (x.double().numpy() for x in res)
+        assert np.abs(o - o_r[pos]).max() <= 2e-2
+        assert np.abs(lse - l_r[:, pos]).max() <= 1e-2
+        for g, ref in ((dq, dq_r), (dk, dk_r), (dv, dv_r)):
+            assert np.abs(g - ref[pos]).max() / np.abs(ref).max() <= 2e-2
 
 
 def _proj_worker(rank, world, port, C, N, causal, q):
@@ -230,7 +261,7 @@ def _stress_worker(rank, world, port, C, q):
 
 @pytest.mark.gpu
 @pytest.mark.multigpu
-@pytest.mark.parametrize("C", [1, 2])
+@pytest.mark.parametrize("C", [1, 2, 4])
 def test_back_to_back_calls_reproducible(C):
     """Repeated fwd+bwd without host synchronisation: the forward is bit-identical across
     calls and the gradients agree up to bf16 rounding of the fp32 reduction order (guards the ring-slot
