@@ -83,3 +83,23 @@ def test_predict_sanity():
     slow = cm.predict(8, 1, 131072, 32, 128, True, 850, 1000, link_gbps=10)
     fast = cm.predict(8, 1, 131072, 32, 128, True, 850, 1000, link_gbps=1e6, latency_us=0)
     assert slow["total_ms"] > fast["total_ms"] and fast["exposed_comm_frac"] < 0.01
+
+
+def test_predict_unit_pipelined_reductions():
+    # extension regime (C^2 > P): of the C-1 member partials only the sender's last unit is
+    # exposed after the pass; the rest travel during later units
+    P, C, N, h, d = 4, 4, 65536, 32, 128
+    r = cm.predict(P, C, N, h, d, True, 1000, 1000, link_gbps=100.0, latency_us=0)
+    by = cm.schedule_bytes(P, C, N, h, d)
+    for pas, name in ((0, "fwd"), (1, "bwd")):
+        rs = max(sum(b for (p, k), b in dct.items() if p == pas and k in ("RS_O", "RS_LSE", "RS_DQ"))
+                 for dct in by.values())
+        rest = max(sum(b for (p, k), b in dct.items() if p == pas and k in ("RET_DQ", "REV_DKV"))
+                   for dct in by.values())
+        want = (rest + rs / (C - 1)) / 100e9 * 1e3
+        assert abs(r[name]["post_ms"] - want) < 1e-9, (name, r[name]["post_ms"], want)
+    # C = 2 at P = 2 has one partial per owner: all of it is exposed
+    r2 = cm.predict(2, 2, 32768, h, d, True, 1000, 1000, link_gbps=100.0, latency_us=0)
+    by2 = cm.schedule_bytes(2, 2, 32768, h, d)
+    rs2 = max(sum(b for (p, k), b in dct.items() if p == 0 and k in ("RS_O", "RS_LSE")) for dct in by2.values())
+    assert abs(r2["fwd"]["post_ms"] - rs2 / 100e9 * 1e3) < 1e-9
