@@ -215,9 +215,13 @@ def simulate_forward(Q, K, V, P, C, causal, compute=True, heads=None, head_dim=N
 
 
 def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=None, head_dim=None, net=None,
-                      direct=False):
+                      direct=False, log=None):
     """Backward of the schedule.  O, LSE: final forward outputs (global order).
     direct: the DIRECT-PULL init variant (see simulate_forward) for the stationary block.
+    log: optional dict; receives the bookkeeping the coverage pins check:
+      "visits"  list of (rank, step, query team, key units) of every block_bwd call;
+      "dq_home" list of (rank, team) of every dQ partial that reached its final holder;
+      "dkv"     {unit: number of dK/dV replica partials its owner summed}.
 
     Returns (dQ, dK, dV, events).
     """
@@ -302,6 +306,8 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
         for s in range(R):
             for r in range(P):
                 pk, st = pkg[r], stat[r]
+                if log is not None:
+                    log.setdefault("visits", []).append((r, s, pk["team"], tuple(range(st["b"] * C, st["b"] * C + C))))
                 if compute:
                     q, do, lse, dd = pk["data"]
                     dq, dk, dv = block_bwd(q, st["kv"][0], st["kv"][1], do, lse, dd, pk["qpos"], st["kpos"], causal)
@@ -326,11 +332,15 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
                 _, (tm, dq) = net.recv("RET_DQ", R - 1, lst[r], r)
                 if tm != r // C:
                     raise RuntimeError("return hop did not bring dQ home")
+                if log is not None:
+                    log.setdefault("dq_home", []).append((r, tm))
                 dq_part[r] = dq
         else:
             for r in range(P):
                 if pkg[r]["team"] != r // C:
                     raise RuntimeError("R=1 package is not the own team")
+                if log is not None:
+                    log.setdefault("dq_home", []).append((r, pkg[r]["team"]))
                 dq_part[r] = pkg[r]["dq"]
         # dK/dV (reading c11, revised): every holder of a stationary team block sends each
         # unit's rows of its fp32 partial straight to the unit's owner, which sums the C
@@ -358,6 +368,9 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
             units = _slice_units(a, P, C)
             kvs = [net.recv("SLICE_KV", -1, u, r)[1] for u in units]
             e = team[r]
+            if log is not None:
+                log.setdefault("visits", []).append((r, 0, r // C, tuple(units)))
+                log.setdefault("dq_home", []).append((r, r // C))
             if compute:
                 k = np.concatenate([x[0] for x in kvs])
                 v = np.concatenate([x[1] for x in kvs])
@@ -377,6 +390,8 @@ def simulate_backward(Q, K, V, dO, O, LSE, P, C, causal, compute=True, heads=Non
                     contrib[u].append(net.recv("REV_DKV", R, r, u)[1])
         dkv_part = contrib
 
+    if log is not None:
+        log["dkv"] = {u: len(contrib[u]) for u in range(P)}
     # Team reduce-scatter sum of dQ.
     for r in range(P):
         t = r // C

@@ -291,3 +291,59 @@ def test_direct_pull_variant_equals_dense(P, C):
         want = {u for u in range(blk * C, blk * C + C) if u != r}
         got = {e.src for e in ev_f if e.kind == "SLICE_KV" and e.dst == r}
         assert got == want
+
+
+# ---- backward bookkeeping pins (independent of the oracle's own byte formulas) -----
+
+def _mib_by_kind(ev, rank, pas):
+    t = trace_totals(ev, rank=rank, pas=pas)
+    assert all(v % 2 ** 20 == 0 for v in t.values())
+    return {k: v // 2 ** 20 for k, v in t.items()}
+
+
+def test_backward_bytes_golden_gpt128k_p8():
+    # SURVEY.md:512-519: received MiB per rank at GPT-128K, P=8 (C=2 and C=1), from an
+    # independent emulator of PAPER.md:169-188 / 201-205.  Fails if dQ travels as bf16,
+    # if the dQ return hop is dropped, or if the package loses LSE/D.
+    gold = json.load(open(os.path.join(GOLD, "bytes_gpt128k_p8.json")))
+    cfg = gold["config"]
+    N, h, d, P = cfg["N"], cfg["heads"], cfg["head_dim"], cfg["P"]
+    for C, key in ((2, "C2"), (1, "C1")):
+        g = gold[key]
+        _, _, evf, _ = simulate_forward(N, None, None, P, C, True, compute=False, heads=h, head_dim=d)
+        _, _, _, evb = simulate_backward(N, None, None, None, None, None, P, C, True, compute=False, heads=h,
+                                         head_dim=d)
+        for r in range(P):
+            f = _mib_by_kind(evf, r, 0)
+            b = _mib_by_kind(evb, r, 1)
+            for kind, mib in g["fwd"].items():
+                assert f.get(kind, 0) == mib, (C, r, "fwd", kind, f.get(kind))
+            for kind, mib in g["bwd"].items():
+                assert b.get(kind, 0) == mib, (C, r, "bwd", kind, b.get(kind))
+            if "INIT_KV" in g:
+                want = 0 if r in g["INIT_KV"]["ranks_zero"] else g["INIT_KV"]["other"]
+                assert f.get("INIT_KV", 0) == want and b.get("INIT_KV", 0) == want, (C, r)
+
+
+@pytest.mark.parametrize("P,C", [(P, C) for P, C in valid_pairs(16)] + [(32, 4), (64, 4), (64, 8)])
+def test_backward_coverage_invariants(P, C):
+    # every (query team, key unit) pair is visited exactly once over the
+    # ring (the backward "mirrors" the forward's coverage), every team's dQ ends at its home
+    # once per member (P:205's return hop), and each unit owner sums exactly C dK/dV
+    # replicas in the paper regime (one per team member holding the stationary block,
+    # reading c11) or T = P/C in the extension (one per team, reading c2).
+    log = {}
+    simulate_backward(2 * P * 4, None, None, None, None, None, P, C, True, compute=False, heads=1, head_dim=2,
+                      log=log)
+    T = P // C
+    seen = {}
+    for r, s, team, units in log["visits"]:
+        for u in units:
+            seen[(team, u)] = seen.get((team, u), 0) + 1
+    # each team has C members; each member covers its share of the keys, so every
+    # (team, unit) pair is visited once by the team as a whole
+    assert sorted(seen) == [(t, u) for t in range(T) for u in range(P)]
+    assert set(seen.values()) == {1}, (P, C)
+    assert sorted(log["dq_home"]) == [(r, r // C) for r in range(P)]
+    want = C if C * C <= P else T
+    assert log["dkv"] == {u: want for u in range(P)}
