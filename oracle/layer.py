@@ -1,27 +1,40 @@
-"""fp64 oracle of the WallFacer Transformer layer (the GPT-7B-style
-block of P:337/P:407: RMSNorm -> QKV projection -> exact attention (Eq. 1) -> output
-projection -> residual -> RMSNorm -> SwiGLU MLP -> residual).
+"""fp64 oracle of the WallFacer Transformer layer.
+
+PAPER.md:199: "The output of this forward attention block is finalized after a standard
+LayerNorm and FeedForward layer process"; P:337 places the checkpoint at the end of the
+self-attention phase.  Reading c22: a pre-LN GPT block --
+    a  = LayerNorm1(x)                          (nn.LayerNorm: affine weight and bias)
+    x1 = x + Attention(a Wqkv^T) Wo^T           (exact attention, Eq. 1)
+    b  = LayerNorm2(x1)
+    y  = x1 + GELU(b W1^T) W2^T                 (FeedForward: Linear H->F, GELU, Linear F->H)
+with the exact (erf) GELU, F = 4H by default, and no linear biases (the paper names none).
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 Written as the plain definitions in PyTorch fp64 CPU ops, gradients by torch.autograd (a
 library primitive).  The sequence parallelism does not change the function: the oracle
 is the layer on the whole sequence.  Pins (tests/test_oracle_layer.py): the attention
-part equals oracle.dense.attention_fwd, RMSNorm / SwiGLU closed forms, and central finite
-differences of the whole layer's gradients.
+part equals oracle.dense.attention_fwd, LayerNorm / GELU closed forms and textbook values,
+and central finite differences of the whole layer's gradients.
 """
+import math
+
 import numpy as np
 import torch
 
-
-def rmsnorm(x, w, eps):
-    return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * w
+WEIGHTS = ("ln1_w", "ln1_b", "wqkv", "wo", "ln2_w", "ln2_b", "w1", "w2")
 
 
-def swiglu(gu):
-    F = gu.shape[-1] // 2
-    g, u = gu[..., :F], gu[..., F:]
-    return g * torch.sigmoid(g) * u
+def layernorm(x, w, b, eps):
+    """(x - mean) / sqrt(var + eps) * w + b, mean and biased variance over the last axis."""
+    mu = x.mean(-1, keepdim=True)
+    var = ((x - mu) ** 2).mean(-1, keepdim=True)
+    return (x - mu) / torch.sqrt(var + eps) * w + b
+
+
+def gelu(u):
+    """u * Phi(u), Phi the standard normal CDF (exact form)."""
+    return u * 0.5 * (1.0 + torch.erf(u / math.sqrt(2.0)))
 
 
 def attention(q, k, v, causal):
@@ -34,16 +47,16 @@ def attention(q, k, v, causal):
 
 
 def layer_forward(x, W, heads, head_dim, causal, eps=1e-5):
-    """x [N, H] fp64 torch; W dict of fp64 torch weights (norm1, wqkv, wo, norm2, w13, w2)."""
+    """x [N, H] fp64 torch; W dict of fp64 torch weights (WEIGHTS)."""
     N = x.shape[0]
     E = heads * head_dim
-    a = rmsnorm(x, W["norm1"], eps)
+    a = layernorm(x, W["ln1_w"], W["ln1_b"], eps)
     qkv = a @ W["wqkv"].T
     q, k, v = (qkv[:, i * E:(i + 1) * E].reshape(N, heads, head_dim) for i in range(3))
     o = attention(q, k, v, causal).reshape(N, E)
     x1 = x + o @ W["wo"].T
-    b = rmsnorm(x1, W["norm2"], eps)
-    return x1 + swiglu(b @ W["w13"].T) @ W["w2"].T
+    b = layernorm(x1, W["ln2_w"], W["ln2_b"], eps)
+    return x1 + gelu(b @ W["w1"].T) @ W["w2"].T
 
 
 def layer_grads(x, W, dy, heads, head_dim, causal, eps=1e-5):

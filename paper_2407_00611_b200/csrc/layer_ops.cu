@@ -1,8 +1,9 @@
 // layer_ops.cu -- the non-GEMM operators of a WallFacer Transformer layer (SURVEY.md §8(f)
-// item 3: the GPT-7B-style block the paper trains): RMSNorm forward/backward,
-// SwiGLU forward/backward, the residual add and the packing of (dQ, dK, dV) into one
-// [rows, 3E] operand for the projection's backward GEMMs.  All HBM-bound: 16-byte vector
-// accesses, one CTA per row for the normalisations (a row is 8 KB at hidden 4096).
+// item 3; "finalized after a standard LayerNorm and FeedForward layer process"):
+// LayerNorm forward/backward, the FeedForward layer's GELU forward/backward, the residual
+// add and the packing of (dQ, dK, dV) into one [rows, 3E] operand for the projection's
+// backward GEMMs.  All HBM-bound: 16-byte vector accesses, one CTA per row for the
+// normalisations (a row is 8 KB at hidden 4096).
 #include <cstdint>
 #include <cstdio>
 
@@ -47,90 +48,118 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 constexpr int kNormThreads = 256;
+constexpr int kMaxV = 4;  // 16-byte vectors per thread: hidden <= 8 * 256 * 4 = 8192
 
-// y = x * rstd * w, rstd = 1 / sqrt(mean(x^2) + eps)   (one CTA per row)
-__global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ w,
-                                                                   bf16* __restrict__ y, float* __restrict__ rstd,
-                                                                   int H, float eps) {
+// LayerNorm (nn.LayerNorm with affine weight and bias; "a standard LayerNorm"):
+// y = (x - mean) rstd w + b, rstd = 1 / sqrt(var + eps), var the biased row variance.
+// One CTA per row; the row stays in registers between the two reductions.
+__global__ void __launch_bounds__(kNormThreads) layernorm_fwd_kernel(const bf16* __restrict__ x,
+                                                                     const bf16* __restrict__ w,
+                                                                     const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                                     float* __restrict__ mean_out,
+                                                                     float* __restrict__ rstd_out, int H, float eps) {
   __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * H);
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* yr = reinterpret_cast<uint4*>(y + row * H);
   const int nv = H / 8;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < nv; i += kNormThreads) {
-    float f[8];
-    unpack8(xr[i], f);
+  float f[kMaxV][8];
+  float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ss += f[k] * f[k];
+  for (int v = 0; v < kMaxV; ++v) {
+    const int i = threadIdx.x + v * kNormThreads;
+    if (i < nv) {
+      unpack8(xr[i], f[v]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += f[v][k];
+    }
+  }
+  const float mu = block_sum<kNormThreads>(s, red) / H;
+  float ss = 0.f;
+#pragma unroll
+  for (int v = 0; v < kMaxV; ++v) {
+    const int i = threadIdx.x + v * kNormThreads;
+    if (i < nv)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float t = f[v][k] - mu;
+        ss += t * t;
+      }
   }
   const float r = rsqrtf(block_sum<kNormThreads>(ss, red) / H + eps);
-  if (threadIdx.x == 0) rstd[row] = r;
-  for (int i = threadIdx.x; i < nv; i += kNormThreads) {
-    float f[8], g[8];
-    unpack8(xr[i], f);
-    unpack8(wr[i], g);
+  if (threadIdx.x == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = r;
+  }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = f[k] * r * g[k];
-    yr[i] = pack8(f);
+  for (int v = 0; v < kMaxV; ++v) {
+    const int i = threadIdx.x + v * kNormThreads;
+    if (i < nv) {
+      float g[8], bb[8], o[8];
+      unpack8(reinterpret_cast<const uint4*>(w)[i], g);
+      unpack8(reinterpret_cast<const uint4*>(b)[i], bb);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = (f[v][k] - mu) * r * g[k] + bb[k];
+      yr[i] = pack8(o);
+    }
   }
 }
 
-// dx = r (w o dy) - x r^3 mean(w o dy o x);  dw += sum_rows dy o x r   (fp32, atomics per CTA)
-__global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                                   const bf16* __restrict__ w,
-                                                                   const float* __restrict__ rstd,
-                                                                   const bf16* __restrict__ dres, bf16* __restrict__ dx,
-                                                                   float* __restrict__ dw, int rows, int H,
-                                                                   int rows_per_cta) {
+// xhat = (x - mean) rstd, g = w o dy:
+//   dx = rstd (g - mean(g) - xhat mean(g o xhat))  (+ dres: the residual branch's gradient)
+//   dw += sum_rows dy o xhat,  db += sum_rows dy     (fp32; per-CTA partials, one atomic each)
+__global__ void __launch_bounds__(kNormThreads) layernorm_bwd_kernel(
+    const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ w,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* __restrict__ dres,
+    bf16* __restrict__ dx, float* __restrict__ dw, float* __restrict__ db, int rows, int H, int rows_per_cta) {
   __shared__ float red[kNormThreads / 32];
   const int nv = H / 8;
-  // this thread's dw partial: columns 8 i .. 8 i + 7 for i = threadIdx.x + k * kNormThreads
-  constexpr int kMaxV = 4;  // H <= 8 * 256 * 4 = 8192
-  float acc[kMaxV][8];
+  float aw[kMaxV][8], ab[kMaxV][8];
 #pragma unroll
   for (int v = 0; v < kMaxV; ++v)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[v][k] = 0.f;
+    for (int k = 0; k < 8; ++k) aw[v][k] = ab[v][k] = 0.f;
   const int r0 = blockIdx.x * rows_per_cta;
   const int r1 = min(rows, r0 + rows_per_cta);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   for (int64_t row = r0; row < r1; ++row) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * H);
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * H);
-    const float r = rstd[row];
-    float dot = 0.f;
+    const float mu = mean_in[row], r = rstd_in[row];
+    float xh[kMaxV][8], g[kMaxV][8];
+    float sg = 0.f, sgx = 0.f;
 #pragma unroll
     for (int v = 0; v < kMaxV; ++v) {
       const int i = threadIdx.x + v * kNormThreads;
       if (i < nv) {
-        float f[8], g[8], d[8];
+        float f[8], ww[8], d[8];
         unpack8(xr[i], f);
-        unpack8(wr[i], g);
+        unpack8(wr[i], ww);
         unpack8(dyr[i], d);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          dot += g[k] * d[k] * f[k];
-          acc[v][k] += d[k] * f[k] * r;
+          xh[v][k] = (f[k] - mu) * r;
+          g[v][k] = ww[k] * d[k];
+          sg += g[v][k];
+          sgx += g[v][k] * xh[v][k];
+          aw[v][k] += d[k] * xh[v][k];
+          ab[v][k] += d[k];
         }
       }
     }
-    const float m = block_sum<kNormThreads>(dot, red) / H;
+    const float mg = block_sum<kNormThreads>(sg, red) / H;
+    const float mgx = block_sum<kNormThreads>(sgx, red) / H;
     uint4* dxr = reinterpret_cast<uint4*>(dx + row * H);
     const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + row * H) : nullptr;
 #pragma unroll
     for (int v = 0; v < kMaxV; ++v) {
       const int i = threadIdx.x + v * kNormThreads;
       if (i < nv) {
-        float f[8], g[8], d[8], o[8];
-        unpack8(xr[i], f);
-        unpack8(wr[i], g);
-        unpack8(dyr[i], d);
+        float o[8];
         if (rr) unpack8(rr[i], o);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float t = r * g[k] * d[k] - f[k] * r * r * r * m;
+          const float t = r * (g[v][k] - mg - xh[v][k] * mgx);
           o[k] = rr ? o[k] + t : t;
         }
         dxr[i] = pack8(o);
@@ -142,46 +171,39 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* _
     const int i = threadIdx.x + v * kNormThreads;
     if (i < nv)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) atomicAdd(dw + 8 * i + k, acc[v][k]);
+      for (int k = 0; k < 8; ++k) {
+        atomicAdd(dw + 8 * i + k, aw[v][k]);
+        atomicAdd(db + 8 * i + k, ab[v][k]);
+      }
   }
 }
 
-__device__ __forceinline__ float sigmoidf_(float g) { return 1.f / (1.f + __expf(-g)); }
+// GELU (the FeedForward layer's activation, nn.GELU's exact form): h = u Phi(u),
+// Phi(u) = (1 + erf(u / sqrt 2)) / 2;  dh/du = Phi(u) + u phi(u), phi(u) = exp(-u^2/2) / sqrt(2 pi)
+__device__ __forceinline__ float gelu_cdf(float u) { return 0.5f * (1.f + erff(u * 0.70710678118654752f)); }
 
-// gu = [gate | up] per row ([rows, 2F]); h = silu(gate) * up
-__global__ void swiglu_fwd_kernel(const bf16* __restrict__ gu, bf16* __restrict__ h, int64_t rows, int F) {
-  const int64_t nv = rows * (F / 8);
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nv;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = t / (F / 8), c = t % (F / 8);
-    float g[8], u[8], o[8];
-    unpack8(reinterpret_cast<const uint4*>(gu + row * 2 * F)[c], g);
-    unpack8(reinterpret_cast<const uint4*>(gu + row * 2 * F + F)[c], u);
+__global__ void gelu_fwd_kernel(const bf16* __restrict__ u, bf16* __restrict__ h, int64_t nv) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(u)[i], f);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
-    reinterpret_cast<uint4*>(h + row * F)[c] = pack8(o);
+    for (int k = 0; k < 8; ++k) f[k] = f[k] * gelu_cdf(f[k]);
+    reinterpret_cast<uint4*>(h)[i] = pack8(f);
   }
 }
 
-// dgate = dh * up * silu'(gate), dup = dh * silu(gate); silu'(g) = s (1 + g (1 - s)), s = sigmoid(g)
-__global__ void swiglu_bwd_kernel(const bf16* __restrict__ dh, const bf16* __restrict__ gu, bf16* __restrict__ dgu,
-                                  int64_t rows, int F) {
-  const int64_t nv = rows * (F / 8);
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nv;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = t / (F / 8), c = t % (F / 8);
-    float g[8], u[8], d[8], dg[8], du[8];
-    unpack8(reinterpret_cast<const uint4*>(gu + row * 2 * F)[c], g);
-    unpack8(reinterpret_cast<const uint4*>(gu + row * 2 * F + F)[c], u);
-    unpack8(reinterpret_cast<const uint4*>(dh + row * F)[c], d);
+__global__ void gelu_bwd_kernel(const bf16* __restrict__ dh, const bf16* __restrict__ u, bf16* __restrict__ du,
+                                int64_t nv) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float f[8], d[8];
+    unpack8(reinterpret_cast<const uint4*>(u)[i], f);
+    unpack8(reinterpret_cast<const uint4*>(dh)[i], d);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float s = sigmoidf_(g[k]);
-      du[k] = d[k] * g[k] * s;
-      dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
-    }
-    reinterpret_cast<uint4*>(dgu + row * 2 * F)[c] = pack8(dg);
-    reinterpret_cast<uint4*>(dgu + row * 2 * F + F)[c] = pack8(du);
+    for (int k = 0; k < 8; ++k)
+      d[k] *= gelu_cdf(f[k]) + f[k] * 0.39894228040143268f * __expf(-0.5f * f[k] * f[k]);
+    reinterpret_cast<uint4*>(du)[i] = pack8(d);
   }
 }
 
@@ -233,51 +255,52 @@ static wf_status lcheck(const char* what) {
   return WF_OK;
 }
 
-extern "C" wf_status wf_rmsnorm_fwd(const void* x, const void* w, int64_t rows, int hidden, float eps, void* y,
-                                    float* rstd, void* stream) {
-  if (!x || !w || !y || !rstd) return lerr(WF_ERR_ARG, "wf_rmsnorm_fwd: null pointer");
-  if (!al16(x) || !al16(w) || !al16(y)) return lerr(WF_ERR_ARG, "wf_rmsnorm_fwd: 16-byte alignment");
-  if (rows < 0 || hidden <= 0 || hidden % 8) return lerr(WF_ERR_CONFIG, "wf_rmsnorm_fwd: hidden % 8 != 0");
+extern "C" wf_status wf_layernorm_fwd(const void* x, const void* w, const void* b, int64_t rows, int hidden,
+                                      float eps, void* y, float* mean, float* rstd, void* stream) {
+  if (!x || !w || !b || !y || !mean || !rstd) return lerr(WF_ERR_ARG, "wf_layernorm_fwd: null pointer");
+  if (!al16(x) || !al16(w) || !al16(b) || !al16(y)) return lerr(WF_ERR_ARG, "wf_layernorm_fwd: 16-byte alignment");
+  if (rows < 0 || hidden <= 0 || hidden % 8 || hidden > 8 * kNormThreads * kMaxV)
+    return lerr(WF_ERR_CONFIG, "wf_layernorm_fwd: hidden % 8 != 0 or hidden > 8192");
   if (rows == 0) return WF_OK;
-  rmsnorm_fwd_kernel<<<static_cast<unsigned>(rows), kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const bf16*>(x), static_cast<const bf16*>(w), static_cast<bf16*>(y), rstd, hidden, eps);
-  return lcheck("rmsnorm_fwd");
+  layernorm_fwd_kernel<<<static_cast<unsigned>(rows), kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), static_cast<const bf16*>(w), static_cast<const bf16*>(b), static_cast<bf16*>(y),
+      mean, rstd, hidden, eps);
+  return lcheck("layernorm_fwd");
 }
 
-extern "C" wf_status wf_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dres,
-                                    int64_t rows, int hidden, void* dx, float* dw, void* stream) {
-  if (!dy || !x || !w || !rstd || !dx || !dw) return lerr(WF_ERR_ARG, "wf_rmsnorm_bwd: null pointer");
+extern "C" wf_status wf_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean,
+                                      const float* rstd, const void* dres, int64_t rows, int hidden, void* dx,
+                                      float* dw, float* db, void* stream) {
+  if (!dy || !x || !w || !mean || !rstd || !dx || !dw || !db) return lerr(WF_ERR_ARG, "wf_layernorm_bwd: null pointer");
   if (!al16(dy) || !al16(x) || !al16(w) || !al16(dx) || (dres && !al16(dres)))
-    return lerr(WF_ERR_ARG, "wf_rmsnorm_bwd: 16-byte alignment");
-  if (rows < 0 || hidden <= 0 || hidden % 8 || hidden > 8 * kNormThreads * 4)
-    return lerr(WF_ERR_CONFIG, "wf_rmsnorm_bwd: hidden % 8 != 0 or hidden > 8192");
+    return lerr(WF_ERR_ARG, "wf_layernorm_bwd: 16-byte alignment");
+  if (rows < 0 || hidden <= 0 || hidden % 8 || hidden > 8 * kNormThreads * kMaxV)
+    return lerr(WF_ERR_CONFIG, "wf_layernorm_bwd: hidden % 8 != 0 or hidden > 8192");
   if (rows == 0) return WF_OK;
   const int per = static_cast<int>((rows + 148 * 4 - 1) / (148 * 4));
   const unsigned grid = static_cast<unsigned>((rows + per - 1) / per);
-  rmsnorm_bwd_kernel<<<grid, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const bf16*>(dy), static_cast<const bf16*>(x), static_cast<const bf16*>(w), rstd,
-      static_cast<const bf16*>(dres), static_cast<bf16*>(dx), dw, static_cast<int>(rows), hidden, per);
-  return lcheck("rmsnorm_bwd");
+  layernorm_bwd_kernel<<<grid, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(dy), static_cast<const bf16*>(x), static_cast<const bf16*>(w), mean, rstd,
+      static_cast<const bf16*>(dres), static_cast<bf16*>(dx), dw, db, static_cast<int>(rows), hidden, per);
+  return lcheck("layernorm_bwd");
 }
 
-extern "C" wf_status wf_swiglu_fwd(const void* gu, int64_t rows, int ffn, void* h, void* stream) {
-  if (!gu || !h) return lerr(WF_ERR_ARG, "wf_swiglu_fwd: null pointer");
-  if (!al16(gu) || !al16(h) || ffn % 8) return lerr(WF_ERR_CONFIG, "wf_swiglu_fwd: alignment / ffn % 8");
-  const int64_t nv = rows * (ffn / 8);
-  if (nv == 0) return WF_OK;
-  swiglu_fwd_kernel<<<grid_elems(nv), 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(gu),
-                                                                                    static_cast<bf16*>(h), rows, ffn);
-  return lcheck("swiglu_fwd");
+extern "C" wf_status wf_gelu_fwd(const void* u, int64_t n, void* h, void* stream) {
+  if (!u || !h) return lerr(WF_ERR_ARG, "wf_gelu_fwd: null pointer");
+  if (!al16(u) || !al16(h) || n % 8) return lerr(WF_ERR_CONFIG, "wf_gelu_fwd: alignment / n % 8");
+  if (n == 0) return WF_OK;
+  gelu_fwd_kernel<<<grid_elems(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(u),
+                                                                                   static_cast<bf16*>(h), n / 8);
+  return lcheck("gelu_fwd");
 }
 
-extern "C" wf_status wf_swiglu_bwd(const void* dh, const void* gu, int64_t rows, int ffn, void* dgu, void* stream) {
-  if (!dh || !gu || !dgu) return lerr(WF_ERR_ARG, "wf_swiglu_bwd: null pointer");
-  if (!al16(dh) || !al16(gu) || !al16(dgu) || ffn % 8) return lerr(WF_ERR_CONFIG, "wf_swiglu_bwd: alignment / ffn % 8");
-  const int64_t nv = rows * (ffn / 8);
-  if (nv == 0) return WF_OK;
-  swiglu_bwd_kernel<<<grid_elems(nv), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const bf16*>(dh), static_cast<const bf16*>(gu), static_cast<bf16*>(dgu), rows, ffn);
-  return lcheck("swiglu_bwd");
+extern "C" wf_status wf_gelu_bwd(const void* dh, const void* u, int64_t n, void* du, void* stream) {
+  if (!dh || !u || !du) return lerr(WF_ERR_ARG, "wf_gelu_bwd: null pointer");
+  if (!al16(dh) || !al16(u) || !al16(du) || n % 8) return lerr(WF_ERR_CONFIG, "wf_gelu_bwd: alignment / n % 8");
+  if (n == 0) return WF_OK;
+  gelu_bwd_kernel<<<grid_elems(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(dh), static_cast<const bf16*>(u), static_cast<bf16*>(du), n / 8);
+  return lcheck("gelu_bwd");
 }
 
 extern "C" wf_status wf_add_bf16(const void* a, const void* b, int64_t n, void* y, void* stream) {

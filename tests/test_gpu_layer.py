@@ -6,14 +6,15 @@ import numpy as np
 import pytest
 import torch
 
-from oracle.layer import layer_grads
+from oracle.layer import WEIGHTS, layer_grads
 from oracle.sharding import unit_positions
 from wf_inputs import to_f64
 
 pytestmark = pytest.mark.gpu
 
-# every activation is stored in bf16 between ~12 operators: a few bf16 ulps end to end
-Y_TOL, G_TOL = 2e-2, 4e-2
+# north_star's bound (max-abs / max |ref|) for the output, the input gradient and every
+# weight gradient; every activation is stored in bf16 between ~12 operators
+Y_TOL, G_TOL = 2e-2, 2e-2
 
 
 def _run(P, C, N, H, h, d, F, causal, checkpoint, seed=0):
@@ -34,7 +35,7 @@ def _run(P, C, N, H, h, d, F, causal, checkpoint, seed=0):
     inv = np.argsort(idx)
     out = dict(y=to_f64(y)[inv], dx=to_f64(dx)[inv])
     out.update({k: (v.double().cpu().numpy() if v.dtype == torch.float32 else to_f64(v)) for k, v in grads.items()})
-    Wn = {k: to_f64(getattr(W, k)) for k in ("norm1", "wqkv", "wo", "norm2", "w13", "w2")}
+    Wn = {k: to_f64(getattr(W, k)) for k in WEIGHTS}
     return out, (to_f64(x), Wn, to_f64(dy))
 
 
@@ -53,7 +54,7 @@ def _check(out, ref_in, h, d, causal):
 @pytest.mark.parametrize("checkpoint", [True, False])
 def test_layer_single_gpu(causal, checkpoint):
     h, d = 2, 128
-    out, ref_in = _run(1, 1, 512, 256, h, d, 384, causal, checkpoint)
+    out, ref_in = _run(1, 1, 512, 256, h, d, 1024, causal, checkpoint)
     ok, errs = _check(out, ref_in, h, d, causal)
     assert ok, errs
 
@@ -61,7 +62,7 @@ def test_layer_single_gpu(causal, checkpoint):
 @pytest.mark.parametrize("P,C", [(4, 2), (4, 4), (2, 1)])
 def test_layer_emulated(P, C):
     h, d = 2, 128
-    out, ref_in = _run(P, C, 256 * P, 256, h, d, 384, True, True, seed=P + C)
+    out, ref_in = _run(P, C, 256 * P, 256, h, d, 1024, True, True, seed=P + C)
     ok, errs = _check(out, ref_in, h, d, True)
     assert ok, errs
 
@@ -69,8 +70,8 @@ def test_layer_emulated(P, C):
 def test_checkpointing_is_exact():
     # the forward is deterministic: identical; gradients differ only by the order of the
     # fp32 dQ reductions (TMA reduce-add) and of the norm-weight atomics
-    a, _ = _run(4, 2, 1024, 256, 2, 128, 384, True, True, seed=3)
-    b, _ = _run(4, 2, 1024, 256, 2, 128, 384, True, False, seed=3)
+    a, _ = _run(4, 2, 1024, 256, 2, 128, 1024, True, True, seed=3)
+    b, _ = _run(4, 2, 1024, 256, 2, 128, 1024, True, False, seed=3)
     assert np.array_equal(a["y"], b["y"])
     for k in a:
         assert np.abs(a[k] - b[k]).max() <= 1e-2 * np.abs(b[k]).max(), k

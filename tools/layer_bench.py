@@ -1,5 +1,5 @@
 """GPU-box helper: WallFacer Transformer layer (GPT-7B shape: hidden 4096, 32 x 128, FFN
-11008, causal) forward + backward throughput, tokens/s and model TFLOP/s, max over ranks.
+16384 = 4H, causal; LayerNorm + GELU FeedForward) forward + backward throughput, tokens/s and model TFLOP/s, max over ranks.
 
     python tools/layer_bench.py [--N 32768]
     torchrun --nproc-per-node 4 tools/layer_bench.py --N 65536 --C 2
@@ -29,7 +29,7 @@ def main():
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
-    H, h, d, F = 4096, 32, 128, 11008
+    H, h, d, F = 4096, 32, 128, 4 * 4096
     N, P = a.N, world
     n = N // P
     W = LayerWeights.random(H, h, d, F, seed=1)
