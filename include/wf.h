@@ -24,8 +24,11 @@
  *  - Errors: every call returns a wf_status; wf_last_error(ctx) gives the text.
  *    WF_ERR_CONFIG: invalid (P, C) or unsupported shape (head_dim not in {64, 72, 128};
  *    N not a multiple of 128 P (full) or 256 P (causal)).  WF_ERR_ARG: null or
- *    misaligned pointer.  WF_ERR_CUDA / WF_ERR_COMM: a CUDA or NCCL failure; the
- *    context should then be finalized.  (Mirrors SPEC.md:524 exit codes 0/1/2.)
+ *    misaligned pointer.  WF_ERR_CUDA: a CUDA failure.  WF_ERR_COMM: a bootstrap
+ *    failure, or -- asynchronously -- a peer that stopped signalling: a wait of an
+ *    earlier call timed out (wf_set_timeout, default 30 s), so the next wf_attn_fwd /
+ *    wf_attn_bwd / wf_qkv_proj returns WF_ERR_COMM (sticky).  After WF_ERR_CUDA or
+ *    WF_ERR_COMM the context should be finalized.  (Mirrors SPEC.md:524 exit codes 0/1/2.)
  */
 #ifndef WF_H_
 #define WF_H_
@@ -79,9 +82,28 @@ wf_status wf_get_uid(wf_uid* out);
 
 /* Create this rank's context: validates (P, C) (reading c2: C | P and, when C^2 <= P,
  * C^2 | P; C^2 > P is the extension regime with R = 1), builds the plan (Alg. 2/3),
- * creates the NCCL communicator on the current CUDA device.  uid: host memory, the
- * same bytes on every rank; may be NULL when P == 1.  out: receives the context. */
+ * creates the bootstrap NCCL communicator on the current CUDA device (used only to
+ * exchange the workspaces' CUDA IPC handles; every message of the schedule then moves
+ * over peer memory).  uid: host memory, the same bytes on every rank; may
+ * be NULL when P == 1.  out: receives the context.  P <= 64. */
 wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, wf_ctx** out);
+
+/* Host all-gather supplied by the caller: every rank passes `bytes` bytes at `in` (host
+ * memory) and receives the P contributions rank-major at `out` (P * bytes); blocking,
+ * collective; returns 0 on success.  `user` is passed through. */
+typedef int (*wf_allgather_fn)(const void* in, void* out, size_t bytes, void* user);
+
+/* As wf_init, with the IPC-handle exchange done by the caller's host collective instead of
+ * NCCL (e.g. torch.distributed over gloo).  Needs no NCCL communicator, so several ranks
+ * may share one GPU (each its own process): the real peer-memory transport can be tested
+ * on a single device.  allgather may be NULL when P == 1; it is called from inside the
+ * first wf_attn_fwd / wf_attn_bwd / wf_qkv_proj of a new shape (collective). */
+wf_status wf_init_bootstrap(int P, int C, wf_topology topo, int rank, wf_allgather_fn allgather, void* user,
+                            wf_ctx** out);
+
+/* Timeout of every inter-rank wait of this context (default 30 s).  A wait that times out
+ * is reported as WF_ERR_COMM by the next call (see Errors).  seconds > 0. */
+wf_status wf_set_timeout(wf_ctx* ctx, double seconds);
 
 /* Single-GPU emulation of all P ranks (test/bench aid): the same schedule, block
  * kernels and trace, with every message a device-local copy.  In this mode every
@@ -208,23 +230,27 @@ wf_status wf_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* 
 wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int b_mn, int M, int N, int K, void* Y,
                          void* stream);
 
-/* ---- the other operators of a WallFacer Transformer layer (SURVEY.md §8(f) item 3,
- * the GPT-7B-style block of P:337/P:407, driven by paper_2407_00611_b200/layer.py) ----
+/* ---- the other operators of a WallFacer Transformer layer (
+ * P:199 "finalized after a standard LayerNorm and FeedForward layer process", driven by
+ * paper_2407_00611_b200/layer.py; reading c22) ----
  * All bf16 row-major device buffers, 16-byte aligned; status as above.
- * wf_rmsnorm_fwd: y = x * rstd * w, rstd[row] = 1/sqrt(mean(x^2) + eps) (fp32 out).
- * wf_rmsnorm_bwd: dx = rstd (w o dy) - x rstd^3 mean(w o dy o x) (+ dres if non-NULL: the
- *   residual branch's gradient), dw += sum_rows dy o x rstd (fp32, accumulated: zero it
- *   first).  hidden <= 8192.
- * wf_swiglu_fwd: gu = [gate | up] ([rows, 2 ffn]) -> h = silu(gate) o up ([rows, ffn]).
- * wf_swiglu_bwd: dh -> dgu = [dh o up o silu'(gate) | dh o silu(gate)].
+ * wf_layernorm_fwd: y = (x - mean) rstd w + b per row (nn.LayerNorm, affine), mean and
+ *   rstd = 1/sqrt(var + eps) fp32 [rows] out (var biased).  hidden % 8 == 0, <= 8192.
+ * wf_layernorm_bwd: with xhat = (x - mean) rstd, g = w o dy:
+ *   dx = rstd (g - mean(g) - xhat mean(g o xhat)) (+ dres if non-NULL: the residual
+ *   branch's gradient); dw += sum_rows dy o xhat, db += sum_rows dy (fp32 [hidden],
+ *   accumulated: zero them first).
+ * wf_gelu_fwd: h = u Phi(u) elementwise (exact erf GELU, the FeedForward activation);
+ *   n elements, n % 8 == 0.
+ * wf_gelu_bwd: du = dh o (Phi(u) + u phi(u)).
  * wf_add_bf16: y = a + b (n elements, n % 8 == 0).
  * wf_pack3_bf16: y [rows, 3E] = [a | b | c] (a, b, c [rows, E]). */
-wf_status wf_rmsnorm_fwd(const void* x, const void* w, int64_t rows, int hidden, float eps, void* y, float* rstd,
-                         void* stream);
-wf_status wf_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, const void* dres,
-                         int64_t rows, int hidden, void* dx, float* dw, void* stream);
-wf_status wf_swiglu_fwd(const void* gu, int64_t rows, int ffn, void* h, void* stream);
-wf_status wf_swiglu_bwd(const void* dh, const void* gu, int64_t rows, int ffn, void* dgu, void* stream);
+wf_status wf_layernorm_fwd(const void* x, const void* w, const void* b, int64_t rows, int hidden, float eps, void* y,
+                           float* mean, float* rstd, void* stream);
+wf_status wf_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
+                           const void* dres, int64_t rows, int hidden, void* dx, float* dw, float* db, void* stream);
+wf_status wf_gelu_fwd(const void* u, int64_t n, void* h, void* stream);
+wf_status wf_gelu_bwd(const void* dh, const void* u, int64_t n, void* du, void* stream);
 wf_status wf_add_bf16(const void* a, const void* b, int64_t n, void* y, void* stream);
 wf_status wf_pack3_bf16(const void* a, const void* b, const void* c, int64_t rows, int E, void* y, void* stream);
 

@@ -32,14 +32,16 @@ _SIGS = {
     "wf_get_uid": (c_int, [ctypes.POINTER(WfUid)]),
     "wf_init": (c_int, [c_int, c_int, c_int, c_int, ctypes.POINTER(WfUid), ctypes.POINTER(c_p)]),
     "wf_init_emulated": (c_int, [c_int, c_int, ctypes.POINTER(c_p)]),
+    "wf_init_bootstrap": (c_int, [c_int, c_int, c_int, c_int, c_p, c_p, ctypes.POINTER(c_p)]),
+    "wf_set_timeout": (c_int, [c_p, ctypes.c_double]),
     "wf_attn_fwd": (c_int, [c_p, c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_p, c_p, c_p]),
     "wf_qkv_proj": (c_int, [c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
     "wf_gemm_bf16": (c_int, [c_p, c_p, c_int, c_int, c_int, c_p, c_p]),
     "wf_gemm_bf16_t": (c_int, [c_p, c_int, c_p, c_int, c_int, c_int, c_int, c_p, c_p]),
-    "wf_rmsnorm_fwd": (c_int, [c_p, c_p, c_i64, c_int, ctypes.c_float, c_p, c_p, c_p]),
-    "wf_rmsnorm_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_p, c_p, c_p]),
-    "wf_swiglu_fwd": (c_int, [c_p, c_i64, c_int, c_p, c_p]),
-    "wf_swiglu_bwd": (c_int, [c_p, c_p, c_i64, c_int, c_p, c_p]),
+    "wf_layernorm_fwd": (c_int, [c_p, c_p, c_p, c_i64, c_int, ctypes.c_float, c_p, c_p, c_p, c_p]),
+    "wf_layernorm_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_p, c_p, c_p, c_p]),
+    "wf_gelu_fwd": (c_int, [c_p, c_i64, c_p, c_p]),
+    "wf_gelu_bwd": (c_int, [c_p, c_p, c_i64, c_p, c_p]),
     "wf_add_bf16": (c_int, [c_p, c_p, c_i64, c_p, c_p]),
     "wf_pack3_bf16": (c_int, [c_p, c_p, c_p, c_i64, c_int, c_p, c_p]),
     "wf_attn_bwd": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_int, c_int, c_int, c_p, c_p, c_p, c_p]),
@@ -68,6 +70,9 @@ _SIGS = {
 }
 
 EXPORTED = sorted(_SIGS)
+
+# int (*wf_allgather_fn)(const void* in, void* out, size_t bytes, void* user)
+ALLGATHER_FN = ctypes.CFUNCTYPE(c_int, c_p, c_p, ctypes.c_size_t, c_p)
 
 
 def load(path: str = LIB_PATH):

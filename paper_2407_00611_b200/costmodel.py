@@ -100,20 +100,24 @@ def predict(P, C, N, heads, head_dim, causal, fwd_tflops, bwd_tflops, link_gbps=
     step_f, step_b = per_step_bytes(P, C, N, heads, head_dim)
     by = schedule_bytes(P, C, N, heads, head_dim)
 
-    def phase_ms(pas, kinds):
+    def phase_ms(pas, kinds, byte_share=1.0):
+        """Slowest rank's bytes of these kinds at link_gbps (times byte_share) plus one
+        latency per message kind present."""
         worst = max(sum(b for (p, k), b in d.items() if p == pas and k in kinds) for d in by.values())
         nmsg = len([k for k in kinds if any(d.get((pas, k), 0) for d in by.values())])
-        return worst / (link_gbps * 1e9) * 1e3 + (latency_us * 1e-3 * nmsg if worst else 0.0)
+        return byte_share * worst / (link_gbps * 1e9) * 1e3 + (latency_us * 1e-3 * nmsg if worst else 0.0)
 
     lat = latency_us * 1e-3
     res = {"P": P, "C": C, "R": R, "regime": "ext" if ext else "paper"}
     for pas, comp, hop in ((0, comp_f, step_f), (1, comp_b, step_b)):
         pre, post = phase_ms(pas, _PRE), phase_ms(pas, _POST)
         if ext and C > 1:
-            # unit-pipelined: of the C-1 member partials a rank receives, all but the one its
-            # sender finishes last were pushed during later units; only that one is exposed
+            # unit-pipelined (the peer-memory transport, the library's only real-mode one): of
+            # the C-1 member partials a rank receives, all but the one its sender finishes last
+            # were pushed during later units; only that one's bytes are exposed, while every
+            # message kind still pays its latency
             rs = {"RS_O", "RS_LSE", "RS_DQ"}
-            post = phase_ms(pas, _POST - rs) + phase_ms(pas, rs) / (C - 1)
+            post = phase_ms(pas, _POST - rs) + phase_ms(pas, rs, byte_share=1.0 / (C - 1))
         if R > 1:
             per = comp / R
             ring = per + (R - 1) * max(per, hop / (link_gbps * 1e9) * 1e3 + lat)

@@ -50,6 +50,10 @@ enum { B_Q = 0, B_K = 1, B_KE = 4, B_V = 7, B_VE = 9, B_S = 11, B_P = 13, B_OF =
 constexpr int kKStages = 3;
 
 constexpr int kFwdThreads = 12 * 32;  // TMA, MMA, 2 spare, 2 x 4 softmax warps
+constexpr int kRegCtl = 56, kRegSoftmax = 224;
+#ifndef WF_FWD_REGSPLIT
+#define WF_FWD_REGSPLIT 1
+#endif  // 56 + 2 x 224 <= 512 registers per lane slot
 
 // Two 128-row query tiles per CTA share every K/V tile (half the K/V smem traffic per
 // FLOP).  The tensor pipe alternates between them -- PV_0(j-1), S_0(j), PV_1(j-1), S_1(j)
@@ -115,7 +119,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-
+  // register split per SM sub-partition (one warp of each warpgroup shares it): the TMA /
+  // MMA warpgroup keeps kRegCtl, the two softmax warpgroups take the rest (kRegSoftmax), so
+  // a softmax thread holds its 128-column S row without spilling
+  if (warp < 4) {
+#if WF_FWD_REGSPLIT
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegCtl));
+#endif
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
     // lane 0: Q and the K ring (3 stages, freed by the S MMAs); lane 1: the V ring
@@ -212,7 +222,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int t = 0; t < ntile; ++t) mma_commit(&bar[B_OF + t]);
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+#if WF_FWD_REGSPLIT
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegSoftmax));
+#endif
     // ------------------------------------------------------------ softmax + epilogue (tile t)
     const int t = (warp - 4) >> 2;
     const int wq = warp & 3;
@@ -411,16 +425,6 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s) {
   if (a.nq <= 0 || a.nq % WF_TILE || a.nk % WF_TILE) return cudaErrorInvalidValue;
-  if (block_fwd_split_ok(a, D)) return launch_block_fwd_split(tq, tk, tv, a, s);
-  if (a.kbase && a.nk > 0 && block_fwd_pair_ok(a, D)) {
-    CUtensorMap tk64;
-    if (make_tmap_rows_box(&tk64, a.kbase, a.nk, a.heads, D, 64)) {
-      FwdArgs b = a;
-      b.tl = timeline_buffer();
-      b.tl_cta = timeline_cta();
-      return launch_block_fwd_pair(tq, tk64, tv, b, s);
-    }
-  }
   switch (D) {
     case 128: return launch_fwd_d<128>(tq, tk, tv, a, s);
     case 64: return launch_fwd_d<64>(tq, tk, tv, a, s);

@@ -165,20 +165,12 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, int a_mn, int b_mn,
                           cudaStream_t s);
 // CTA-pair (cta_group::2) variant for K-major A and B with M, N, split multiples of 256
-// (WF_GEMM_PAIR=0 disables it); its A and B maps both use 128-row boxes.
+// (used whenever it applies); its A and B maps both use 128-row boxes.
 bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn);
 cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
-// split-row forward (attn_fwd3.cu): head_dim 128, two softmax threads per row (WF_FWD_SPLIT=1)
-bool block_fwd_split_ok(const FwdArgs& a, int D);
-cudaError_t launch_block_fwd_split(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                   const FwdArgs& a, cudaStream_t s);
-// CTA-pair forward (attn_fwd2.cu): head_dim 128, nq % 512 == 0, opt-in with WF_FWD_PAIR=1
-bool block_fwd_pair_ok(const FwdArgs& a, int D);
-cudaError_t launch_block_fwd_pair(const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv,
-                                  const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                              const CUtensorMap& tdo, const BwdArgs& a, int D, cudaStream_t s);
 
@@ -215,6 +207,10 @@ struct SigArgs {
   int n;
   uint32_t* dst[WF_MAX_SIG];
   uint32_t val[WF_MAX_SIG];
+  // waits only: host-mapped failure words ([0] flag, [1] expected, [2] seen) written on a
+  // timeout of timeout_ns; a wait that finds [0] set returns at once (fail fast)
+  uint32_t* fail;
+  uint64_t timeout_ns;
 };
 cudaError_t launch_signal_wait(const SigArgs& sig, const SigArgs& wait, cudaStream_t s);
 }  // namespace wf

@@ -383,12 +383,7 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
 }
 
 bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("WF_GEMM_PAIR");
-    env = (e && e[0] == '0') ? 0 : 1;
-  }
-  return env && !a_mn && !b_mn && g.M % 256 == 0 && g.N % 256 == 0 && g.split % 256 == 0;
+  return !a_mn && !b_mn && g.M % 256 == 0 && g.N % 256 == 0 && g.split % 256 == 0;
 }
 
 cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {

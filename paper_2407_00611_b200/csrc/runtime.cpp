@@ -1,14 +1,15 @@
 // runtime.cpp -- the C ABI of include/wf.h: context, workspace, and the WallFacer
 // schedule (forward: Alg. 1; backward: PAPER.md:201-205) driving the
-// sm_100a block kernels and the NVLink transport (NCCL P2P on a comm stream).
+// sm_100a block kernels and the NVLink peer-memory transport (copy-engine pushes into the
+// peers' CUDA-IPC-mapped workspaces, release/acquire flags).
 //
 // One schedule implementation serves three modes:
-//   real      : one process per GPU; this rank executes its sends/receives with NCCL
-//               (grouped ncclSend/ncclRecv) and its block kernels; records its sends.
+//   real      : one process per GPU (or, for tests, several processes sharing one GPU);
+//               this rank executes its pushes, waits and block kernels; records its sends.
+//               Bootstrap (the IPC handle exchange) through NCCL (wf_init) or a caller
+//               supplied host all-gather (wf_init_bootstrap).
 //   emulated  : all P ranks on this GPU; every message is a device-local copy.
 //   dry       : no GPU work at all; only the CommTrace is produced (wf_plan_trace).
-// Messages of one phase are issued in one global order (ranks ascending), so the
-// per-peer order of NCCL sends and receives always matches.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -86,11 +87,13 @@ struct wf_ctx {
   int rank = 0;
   bool emulated = false, dry = false;
   int dry_rank = -1;  // dry mode: record only events touching this rank as sender (-1: all)
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;                      // bootstrap only (wf_init)
+  wf_allgather_fn ag_fn = nullptr;                // bootstrap only (wf_init_bootstrap)
+  void* ag_user = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   // workspace
-  int64_t ws_key[4] = {0, 0, 0, 0};
+  int64_t ws_key[5] = {0, 0, 0, 0, 0};
   void* ws = nullptr;
   size_t ws_bytes = 0;
   std::vector<RankBufs> rb;
@@ -98,14 +101,18 @@ struct wf_ctx {
   int64_t launches = 0;
   std::string err;
   int debug = 0;
-  bool emu_unitpipe = false;  // emulated: run the extension regime unit-pipelined (WF_EMU_UNITPIPE=1)
   int sched = WF_SCHED_GATHER_SHUFFLE;  // wf_set_schedule
-  // DIRECT-PULL at R = 1 unit-pipelined (WF_DIRECT_UNITPIPE=1): measured slower at P = 4,
-  // C = 2 than one whole-block launch after the pulls (small launches), so off by default
-  bool direct_unitpipe = false;
-  // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V)
+  // set by wf_qkv_proj when its epilogue already delivered the team gather of (Q, K, V);
+  // consumed only by the wf_attn_fwd that immediately follows it on this context (call
+  // sequence numbers), with the same tensors and geometry
   const void *proj_q = nullptr, *proj_k = nullptr, *proj_v = nullptr;
   int64_t proj_key[4] = {0, 0, 0, 0};
+  uint64_t seq = 0, proj_seq = 0;
+  // asynchronous failure reporting (WF_ERR_COMM): a wait that times out writes these
+  // host-mapped words ([0] = 1, [1] = expected count, [2] = count seen) instead of trapping
+  volatile uint32_t* hfail = nullptr;
+  uint32_t* dfail = nullptr;
+  uint64_t timeout_ns = 30000000000ull;
   // peer-memory transport (real mode, P > 1): CUDA IPC mapped workspaces + flag signalling
   bool ipc = false;
   std::vector<char*> peer_base;
@@ -215,20 +222,33 @@ RankBufs translate(const RankBufs& b, const char* from, const char* to) {
   return t;
 }
 
+// Bootstrap all-gather of `bytes` host bytes per rank (rank-major into out): the caller's
+// host collective (wf_init_bootstrap) or NCCL over the bootstrap communicator (wf_init).
+wf_status boot_allgather(wf_ctx* ctx, const void* in, void* out, size_t bytes) {
+  const int P = ctx->plan.P, me = ctx->rank;
+  if (ctx->ag_fn) {
+    if (ctx->ag_fn(in, out, bytes, ctx->ag_user) != 0) return fail(ctx, WF_ERR_COMM, "bootstrap all-gather failed");
+    return WF_OK;
+  }
+  if (!ctx->comm) return fail(ctx, WF_ERR_COMM, "no bootstrap communicator");
+  void* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, static_cast<size_t>(P) * bytes));
+  CK(cudaMemcpy(static_cast<char*>(dbuf) + me * bytes, in, bytes, cudaMemcpyHostToDevice));
+  NCK(ncclAllGather(static_cast<char*>(dbuf) + me * bytes, dbuf, bytes, ncclInt8, ctx->comm, ctx->comm_stream));
+  CK(cudaStreamSynchronize(ctx->comm_stream));
+  CK(cudaMemcpy(out, dbuf, P * bytes, cudaMemcpyDeviceToHost));
+  CK(cudaFree(dbuf));
+  return WF_OK;
+}
+
 wf_status exchange_ipc(wf_ctx* ctx) {
   const int P = ctx->plan.P, me = ctx->rank;
   for (size_t r = 0; r < ctx->peer_base.size(); ++r)
     if (static_cast<int>(r) != me && ctx->peer_base[r]) cudaIpcCloseMemHandle(ctx->peer_base[r]);
   cudaIpcMemHandle_t h;
   CK(cudaIpcGetMemHandle(&h, ctx->ws));
-  void* dbuf = nullptr;
-  CK(cudaMalloc(&dbuf, static_cast<size_t>(P) * sizeof(h)));
-  CK(cudaMemcpy(static_cast<char*>(dbuf) + me * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice));
-  NCK(ncclAllGather(static_cast<char*>(dbuf) + me * sizeof(h), dbuf, sizeof(h), ncclInt8, ctx->comm, ctx->comm_stream));
-  CK(cudaStreamSynchronize(ctx->comm_stream));
   std::vector<cudaIpcMemHandle_t> hs(P);
-  CK(cudaMemcpy(hs.data(), dbuf, P * sizeof(h), cudaMemcpyDeviceToHost));
-  CK(cudaFree(dbuf));
+  WCK(boot_allgather(ctx, &h, hs.data(), sizeof(h)));
   ctx->peer_base.assign(P, nullptr);
   ctx->rbp.assign(P, RankBufs{});
   for (int r = 0; r < P; ++r) {
@@ -249,10 +269,9 @@ wf_status exchange_ipc(wf_ctx* ctx) {
   ctx->epoch = 0;
   // every rank has zeroed its flags before anyone signals (the all-gather above ordered
   // the memsets; this second one orders the mappings)
-  int32_t* scratch = reinterpret_cast<int32_t*>(static_cast<char*>(ctx->ws) + kFlagBytes - 64);
-  NCK(ncclAllReduce(scratch, scratch, 1, ncclInt32, ncclSum, ctx->comm, ctx->comm_stream));
-  CK(cudaStreamSynchronize(ctx->comm_stream));
-  return WF_OK;
+  int32_t one = me;
+  std::vector<int32_t> all(P);
+  return boot_allgather(ctx, &one, all.data(), sizeof(one));
 }
 
 // flag addresses: data[chan][src] at word chan*64 + src, ack[src] at 128 + src, bar[src] at 192 + src
@@ -263,33 +282,45 @@ uint32_t* flag_of(wf_ctx* ctx, int owner, int word) {
 wf_status ipc_barrier(wf_ctx* ctx, cudaStream_t st);
 
 // ------------------------------------------------------------------ workspace
-// the workspace carve of one rank (bytes per buffer, in carve order)
+// The workspace carve of one rank (bytes per buffer, in carve order), sized by regime:
+// only the buffers this (P, C, R) schedule touches.  `copies`: messages land in receive
+// slots (emulated mode); with peer memory the reductions read the senders' partials in
+// place, so the merge / dQ-sum / dK-dV replica slots exist only where partials are pushed
+// (the unit-pipelined extension regime).
 using CarveList = std::vector<std::pair<void**, int64_t>>;
-void carve_rank(const Geo& g, RankBufs& b, CarveList& items) {
+void carve_rank(const Geo& g, RankBufs& b, CarveList& items, bool copies) {
   const int64_t C = g.C, n = g.n, E = g.E, h = g.h, Bk = g.Bk;
   const int64_t team = C * n * E;  // elements of a team tensor
   auto add = [&](auto** p, int64_t bytes) { items.push_back({reinterpret_cast<void**>(p), bytes}); };
+  const bool pushed = copies || !g.paper;  // partials pushed into their owners' slots
   if (C > 1) {
     add(&b.qt, team * 2);
     add(&b.t_do, team * 2);
     add(&b.t_lse, C * h * n * 4);
     add(&b.t_dsum, C * h * n * 4);
-    add(&b.rs_o, team * 4);
-    add(&b.rs_lse, C * h * n * 4);
-    add(&b.rsq, team * 4);
-    if (g.paper) {
+    if (pushed) {
+      add(&b.rs_o, team * 4);
+      add(&b.rs_lse, C * h * n * 4);
+      add(&b.rsq, team * 4);
+    }
+    if (g.paper && !g.direct) {
       add(&b.kt, team * 2);
       add(&b.vt, team * 2);
     }
   }
-  for (int s = 0; s < 2; ++s) {
+  // K/V receive slots: double-buffered ring (R > 1), one slot for the init block / slice
+  // (R = 1, P > 1), none on one GPU (the caller's K/V are the whole sequence)
+  const int kv_slots = g.R > 1 ? 2 : (g.P > 1 ? 1 : 0);
+  for (int s = 0; s < kv_slots; ++s) {
     add(&b.rk[s], Bk * E * 2);
     add(&b.rv[s], Bk * E * 2);
   }
-  add(&b.o_state, team * 4);
-  add(&b.lse_state, C * h * n * 4);
+  if (g.P > 1) {  // one GPU writes the final bf16 output straight from the block kernel
+    add(&b.o_state, team * 4);
+    add(&b.lse_state, C * h * n * 4);
+  }
   add(&b.dsum, h * n * 4);
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < (g.R > 1 ? 2 : 1); ++s) {
     add(&b.pdq[s], team * 4);
     if (g.R > 1) {
       add(&b.pq[s], team * 2);
@@ -299,9 +330,11 @@ void carve_rank(const Geo& g, RankBufs& b, CarveList& items) {
     }
   }
   if (g.R > 1) add(&b.home_dq, team * 4);
-  add(&b.dk_acc, Bk * E * 4);
-  add(&b.dv_acc, Bk * E * 4);
-  {  // dK/dV replica slots on the owner (holders of a unit: C paper, T extension)
+  if (g.P > 1) {  // one GPU writes bf16 dK/dV straight from the block kernel
+    add(&b.dk_acc, Bk * E * 4);
+    add(&b.dv_acc, Bk * E * 4);
+  }
+  if (copies) {  // dK/dV replica slots on the owner (holders of a unit: C paper, T extension)
     const int64_t slots = g.paper ? C : g.T;
     add(&b.rev_k, slots * n * E * 4);
     add(&b.rev_v, slots * n * E * 4);
@@ -319,8 +352,8 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
     ctx->rb.assign(ctx->plan.P, RankBufs{});
     return WF_OK;
   }
-  const int64_t key[4] = {g.N, g.h, g.d, g.causal};
-  if (ctx->ws && std::equal(key, key + 4, ctx->ws_key)) return WF_OK;
+  const int64_t key[5] = {g.N, g.h, g.d, g.causal, g.direct};
+  if (ctx->ws && std::equal(key, key + 5, ctx->ws_key)) return WF_OK;
   if (ctx->ws) {
     CK(cudaDeviceSynchronize());
     if (ctx->ipc) {
@@ -338,7 +371,7 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   const int nranks = ctx->emulated ? g.P : 1;
   CarveList items;
   std::vector<RankBufs> rb(nranks);
-  for (auto& b : rb) carve_rank(g, b, items);
+  for (auto& b : rb) carve_rank(g, b, items, ctx->emulated);
   const size_t total = carve_total(items);
   void* base = nullptr;
   CK(cudaMalloc(&base, total));
@@ -351,7 +384,7 @@ wf_status ensure_ws(wf_ctx* ctx, const Geo& g) {
   }
   ctx->ws = base;
   ctx->ws_bytes = total;
-  std::copy(key, key + 4, ctx->ws_key);
+  std::copy(key, key + 5, ctx->ws_key);
   ctx->rb = rb;
   if (ctx->ipc) WCK(exchange_ipc(ctx));
   return WF_OK;
@@ -366,6 +399,15 @@ bool addressable(const wf_ctx* ctx, int r) { return local(ctx, r) || (ctx->ipc &
 
 cudaEvent_t pool_event(wf_ctx* ctx);
 cudaEvent_t prof_begin(wf_ctx* ctx, cudaStream_t st);
+
+// Launch a signal/wait kernel whose waits report a timeout through the context's
+// host-mapped failure words (WF_ERR_COMM on the next call) instead of trapping.
+wf_status sigwait(wf_ctx* ctx, SigArgs sig, SigArgs wt, cudaStream_t st) {
+  wt.fail = ctx->dfail;
+  wt.timeout_ns = ctx->timeout_ns;
+  CK(launch_signal_wait(sig, wt, st));
+  return WF_OK;
+}
 
 // ------------------------------------------------------------------ transport
 // part: kPhaseAll, or (peer-memory transport) kPhaseSend = trace + copies + signals only and
@@ -392,67 +434,35 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
     return WF_OK;
   }
   const int me = ctx->rank;
-  if (ctx->ipc) {
-    const int ch = st == ctx->comm_stream ? 1 : 0;
-    cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
-    if (part != kPhaseWait) {
-      for (const Xfer& x : xs) {
-        if (x.src != me || x.pull || x.fused) continue;
-        for (const Seg& sg : x.segs)
-          if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
-      }
-    }
-    SigArgs sig{}, wt{};
-    bool dst_done[kMaxRanks] = {}, src_done[kMaxRanks] = {};
-    for (const Xfer& x : xs) {
-      if (part != kPhaseWait && x.src == me && x.dst != me && !dst_done[x.dst]) {
-        dst_done[x.dst] = true;
-        sig.dst[sig.n] = flag_of(ctx, x.dst, ch * 64 + me);
-        sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
-      }
-      if (part != kPhaseSend && x.dst == me && x.src != me && !src_done[x.src]) {
-        src_done[x.src] = true;
-        wt.dst[wt.n] = flag_of(ctx, me, ch * 64 + x.src);
-        wt.val[wt.n++] = ++ctx->rcvd[ch][x.src];
-      }
-    }
-    CK(launch_signal_wait(sig, wt, st));
-    if (pe0) {
-      cudaEvent_t e1 = pool_event(ctx);
-      cudaEventRecord(e1, st);
-      ctx->ev_phase.push_back({xs[0].kind, {pe0, e1}});
-    }
-    return WF_OK;
-  }
+  const int ch = st == ctx->comm_stream ? 1 : 0;
   cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
-  struct PhaseEnd {
-    wf_ctx* c;
-    cudaStream_t s;
-    cudaEvent_t e0;
-    int kind;
-    ~PhaseEnd() {
-      if (!e0) return;
-      cudaEvent_t e1 = pool_event(c);
-      cudaEventRecord(e1, s);
-      c->ev_phase.push_back({kind, {e0, e1}});
-    }
-  } pend{ctx, st, pe0, xs.empty() ? 0 : xs[0].kind};
-  bool any = false;
-  for (const Xfer& x : xs) any = any || ((x.src == me) != (x.dst == me));
-  if (any) NCK(ncclGroupStart());
-  for (const Xfer& x : xs) {
-    for (const Seg& s : x.segs) {
-      if (!s.bytes) continue;
-      if (x.src == me && x.dst == me) {
-        if (s.src != s.dst) CK(cudaMemcpyAsync(s.dst, s.src, s.bytes, cudaMemcpyDeviceToDevice, st));
-      } else if (x.src == me) {
-        NCK(ncclSend(s.src, static_cast<size_t>(s.bytes), ncclInt8, x.dst, ctx->comm, st));
-      } else if (x.dst == me) {
-        NCK(ncclRecv(s.dst, static_cast<size_t>(s.bytes), ncclInt8, x.src, ctx->comm, st));
-      }
+  if (part != kPhaseWait) {
+    for (const Xfer& x : xs) {
+      if (x.src != me || x.pull || x.fused) continue;
+      for (const Seg& sg : x.segs)
+        if (sg.bytes && sg.src != sg.dst) CK(cudaMemcpyAsync(sg.dst, sg.src, sg.bytes, cudaMemcpyDefault, st));
     }
   }
-  if (any) NCK(ncclGroupEnd());
+  SigArgs sig{}, wt{};
+  bool dst_done[kMaxRanks] = {}, src_done[kMaxRanks] = {};
+  for (const Xfer& x : xs) {
+    if (part != kPhaseWait && x.src == me && x.dst != me && !dst_done[x.dst]) {
+      dst_done[x.dst] = true;
+      sig.dst[sig.n] = flag_of(ctx, x.dst, ch * 64 + me);
+      sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
+    }
+    if (part != kPhaseSend && x.dst == me && x.src != me && !src_done[x.src]) {
+      src_done[x.src] = true;
+      wt.dst[wt.n] = flag_of(ctx, me, ch * 64 + x.src);
+      wt.val[wt.n++] = ++ctx->rcvd[ch][x.src];
+    }
+  }
+  WCK(sigwait(ctx, sig, wt, st));
+  if (pe0) {
+    cudaEvent_t e1 = pool_event(ctx);
+    cudaEventRecord(e1, st);
+    ctx->ev_phase.push_back({xs[0].kind, {pe0, e1}});
+  }
   return WF_OK;
 }
 
@@ -485,7 +495,7 @@ wf_status run_phase_per_source(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<w
       sig.val[sig.n++] = ++ctx->sent[ch][x.dst];
     }
   }
-  CK(launch_signal_wait(sig, none, st));
+  WCK(sigwait(ctx, sig, none, st));
   for (const Xfer& x : xs) {
     if (x.dst == me && x.src != me && !src_done[x.src]) {
       src_done[x.src] = true;
@@ -493,7 +503,7 @@ wf_status run_phase_per_source(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<w
       w.dst[0] = flag_of(ctx, me, ch * 64 + x.src);
       w.val[0] = ++ctx->rcvd[ch][x.src];
       w.n = 1;
-      CK(launch_signal_wait(none, w, st));
+      WCK(sigwait(ctx, none, w, st));
       CK(cudaEventRecord(src_ev[x.src], st));
     }
   }
@@ -558,7 +568,7 @@ wf_status ipc_barrier(wf_ctx* ctx, cudaStream_t st) {
     wt.dst[wt.n] = flag_of(ctx, me, 192 + r);
     wt.val[wt.n++] = ctx->epoch;
   }
-  CK(launch_signal_wait(sig, wt, st));
+  WCK(sigwait(ctx, sig, wt, st));
   return WF_OK;
 }
 // Tell `to` that I finished reading the ring slot it fills (one more released slot).
@@ -568,7 +578,7 @@ wf_status ipc_ack(wf_ctx* ctx, int to, cudaStream_t st) {
   sig.dst[0] = flag_of(ctx, to, 128 + ctx->rank);
   sig.val[0] = ++ctx->acks_sent[to];
   sig.n = 1;
-  CK(launch_signal_wait(sig, wt, st));
+  WCK(sigwait(ctx, sig, wt, st));
   return WF_OK;
 }
 // Wait until `from` has released `count` slots in this ring loop (ack_base counts the
@@ -579,7 +589,7 @@ wf_status ipc_wait_ack(wf_ctx* ctx, int from, uint32_t count, cudaStream_t st) {
   wt.dst[0] = flag_of(ctx, ctx->rank, 128 + from);
   wt.val[0] = ctx->ack_base[from] + count;
   wt.n = 1;
-  CK(launch_signal_wait(sig, wt, st));
+  WCK(sigwait(ctx, sig, wt, st));
   return WF_OK;
 }
 std::vector<cudaEvent_t>& source_events(wf_ctx* ctx, int n) {
@@ -652,8 +662,8 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   tr.clear();
   // gathers already delivered by wf_qkv_proj's epilogue (same tensors, same geometry)
   const int64_t key[4] = {g.N, g.h, g.d, g.causal};
-  const bool pre = ctx->proj_q && ctx->proj_q == Q && ctx->proj_k == K && ctx->proj_v == V &&
-                   std::equal(key, key + 4, ctx->proj_key);
+  const bool pre = ctx->proj_q && ctx->proj_seq + 1 == ctx->seq && ctx->proj_q == Q && ctx->proj_k == K &&
+                   ctx->proj_v == V && std::equal(key, key + 4, ctx->proj_key);
   ctx->proj_q = ctx->proj_k = ctx->proj_v = nullptr;
   WCK(ipc_barrier(ctx, st));
 
@@ -670,7 +680,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   // team(recv[r]) (paper regime; pulled unit by unit in the DIRECT-PULL variant).
   auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
   const int kcount = g.paper ? C : g.W;
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1 && ctx->direct_unitpipe));
+  const bool unitpipe = (ctx->ipc || ctx->emulated) && C > 1 && !g.paper;
   if (unitpipe) {
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));
@@ -868,22 +878,18 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
           x.segs.push_back({slot_v(r, s), lp(dst, B(ctx, dst).rv[(s + 1) & 1]), static_cast<int64_t>(g.Bk) * E * 2});
           xs.push_back(x);
         }
-        if (overlap && ctx->ipc) {
+        if (overlap) {
           // Alg. 1 l.8 with peer copies: the comm stream pushes block s into next's other
           // slot as soon as next has released it (its step s-1), independent of my compute.
           if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
           WCK(run_phase(ctx, xs, tr, ctx->comm_stream, kPhaseSend));
-        } else if (overlap) {  // Alg. 1 l.8: launch the transfer of the next block, then compute
-          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-          WCK(run_phase(ctx, xs, tr, ctx->comm_stream));
-          CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
         }
       }
       for (int r = 0; r < P; ++r)
         if (local(ctx, r)) WCK(compute(r, s));
       if (s < R - 1) {
-        if (overlap && ctx->ipc) {
+        if (overlap) {
           // my slot s is free again once my kernel has read it AND my comm stream has
           // forwarded it to next (the send above): release it from the comm stream after
           // both, then wait for block s+1 from last
@@ -893,19 +899,17 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
           WCK(run_phase(ctx, xs, tr, ctx->comm_stream, kPhaseWait));
           CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
           CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
-        } else if (overlap) {
-          CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
-          CK(cudaEventRecord(ctx->ev_a, st));
         } else {
           WCK(run_phase(ctx, xs, tr, st));
         }
       }
     }
-    if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
+    if (overlap && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
 
   }
 
   // Alg. 1 l.11: ReduceScatter_combine -- partial rows to their owner, LSE-merge there.
+  const bool nt = (ctx->debug & WF_DEBUG_NO_TRANSFER) != 0;
   if (C > 1) {
     std::vector<Xfer> xs;
     for (int r = 0; r < P; ++r) {
@@ -937,7 +941,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       m.nparts = C;
       const int t0 = (r / C) * C;
       for (int i = 0; i < C; ++i) {
-        if (i == j) {
+        if (i == j || nt) {  // own partial (nt: no-transfer timing baseline, local reads only)
           m.o[i] = b.o_state + i * n * E;
           m.lse[i] = b.lse_state + i * h * n;
         } else if (ctx->ipc && (!unitpipe || last_unit_of(C, i, j))) {  // read in place over NVLink
@@ -968,6 +972,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_bwd;
   tr.clear();
+  const bool nt = (ctx->debug & WF_DEBUG_NO_TRANSFER) != 0;
   WCK(ipc_barrier(ctx, st));
 
   // D = rowsum(dO o O) on own rows (reading c12).
@@ -992,14 +997,14 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   for (int r = 0; r < P; ++r) pkg_team[r] = r / C;
   auto kfirst = [&](int r) { return g.paper ? (pl.recv[r] / C) * C : (r % C) * g.W; };
   const int kcount = g.paper ? C : g.W;
-  const bool unitpipe = (ctx->ipc || (ctx->emulated && ctx->emu_unitpipe)) && C > 1 && (!g.paper || (g.direct && R == 1 && ctx->direct_unitpipe));
+  const bool unitpipe = (ctx->ipc || ctx->emulated) && C > 1 && !g.paper;
   if (unitpipe) {
     // Extension regime over peer memory (R = 1): unit-pipelined like the forward.  The
     // gathers of Q, dO, LSE, D and the K/V slice pull run on the comm stream with one
     // completion event per source rank; the step is cut into (query unit, key unit)
     // launches, locally present units first.  dQ rows accumulate per query unit, dK/dV
-    // rows per key unit.  (Emulated mode can run the same decomposition for every
-    // virtual rank, WF_EMU_UNITPIPE=1, so it is tested at every (P, C) on one GPU.)
+    // rows per key unit.  (Emulated mode runs the same decomposition for every virtual
+    // rank, so it is tested at every (P, C) on one GPU.)
     std::vector<cudaEvent_t>& sev = source_events(ctx, P);
     CK(cudaEventRecord(ctx->ev_a, st));  // after D of my rows
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
@@ -1162,14 +1167,11 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           y.segs.push_back({pdq(r, s), lp(dst, B(ctx, dst).pdq[s1]), team * 4});
           dq.push_back(y);
         }
-        if (overlap && ctx->ipc) {
+        if (overlap) {
           // the package does not depend on step s: push it as soon as next released the slot
           if (s == 0) CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
           WCK(ipc_wait_ack(ctx, pl.next[ctx->rank], static_cast<uint32_t>(s), ctx->comm_stream));
           WCK(run_phase(ctx, pk, tr, ctx->comm_stream, kPhaseSend));
-        } else if (overlap) {  // the package does not depend on step s: post it first
-          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0));
-          WCK(run_phase(ctx, pk, tr, ctx->comm_stream));
         }
       }
       for (int r = 0; r < P; ++r) {
@@ -1205,7 +1207,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         prof_end(ctx, st, e0, ctx->ev_bwd);
       }
       if (s < R - 1) {
-        if (overlap && ctx->ipc) {
+        if (overlap) {
           // dQ depends on step s: push it after the step; my package and dQ slots are free
           // once my kernel has read them and both sends have left (comm stream order), so
           // the release goes out from the comm stream after them; then wait for step s+1
@@ -1217,14 +1219,6 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           WCK(run_phase(ctx, dq, tr, ctx->comm_stream, kPhaseWait));
           CK(cudaEventRecord(step_event(ctx, s), ctx->comm_stream));
           CK(cudaStreamWaitEvent(st, step_event(ctx, s), 0));
-        } else if (overlap) {
-          // dQ depends on step s: after it; the receiver's next step waits for both
-          CK(cudaEventRecord(ctx->ev_b, st));
-          CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
-          WCK(run_phase(ctx, dq, tr, ctx->comm_stream));
-          CK(cudaEventRecord(ctx->ev_b, ctx->comm_stream));
-          CK(cudaStreamWaitEvent(st, ctx->ev_b, 0));
-          CK(cudaEventRecord(ctx->ev_a, st));
         } else {
           WCK(run_phase(ctx, pk, tr, st));
           WCK(run_phase(ctx, dq, tr, st));
@@ -1235,7 +1229,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       }
     }
 
-    if (overlap && ctx->ipc && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
+    if (overlap && !(ctx->debug & WF_DEBUG_NO_TRANSFER)) ctx->ack_base[pl.next[ctx->rank]] += R - 1;
 
   }
 
@@ -1288,6 +1282,11 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         const int r = holders[u][i];
         const int64_t o = static_cast<int64_t>(u - first_unit(r)) * n * E;
         const bool own = r == u;
+        if (nt && !own) {  // no-transfer timing baseline: a local accumulator, same bytes
+          kparts[u].push_back(lp(u, B(ctx, u).dk_acc));
+          vparts[u].push_back(lp(u, B(ctx, u).dv_acc));
+          continue;
+        }
         kparts[u].push_back(own || ctx->ipc ? at(lp(r, B(ctx, r).dk_acc), o)
                                             : at(lp(u, B(ctx, u).rev_k), static_cast<int64_t>(i) * n * E));
         vparts[u].push_back(own || ctx->ipc ? at(lp(r, B(ctx, r).dv_acc), o)
@@ -1318,7 +1317,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
     for (int i = 0; i < C; ++i) {
       const int ri = (r / C) * C + i;
       const bool in_place = ctx->ipc && (!unitpipe || last_unit_of(C, i, j));
-      qparts[r].push_back(i == j     ? at(home[r], i * n * E)
+      qparts[r].push_back(i == j || nt ? at(home[r], i * n * E)
                           : in_place ? at(home[ri], j * n * E)
                                      : at(lp(r, B(ctx, r).rsq), i * n * E));
     }
@@ -1359,7 +1358,31 @@ wf_status make_streams(wf_ctx* ctx) {
   CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
+  void* hf = nullptr;
+  CK(cudaHostAlloc(&hf, 64, cudaHostAllocMapped));
+  std::memset(hf, 0, 64);
+  ctx->hfail = static_cast<volatile uint32_t*>(hf);
+  void* df = nullptr;
+  CK(cudaHostGetDevicePointer(&df, hf, 0));
+  ctx->dfail = static_cast<uint32_t*>(df);
   return WF_OK;
+}
+
+// WF_ERR_COMM once a wait of an earlier call timed out (a peer stopped signalling): the
+// failure is sticky, the context must be finalized.
+wf_status comm_ok(wf_ctx* ctx) {
+  if (!ctx->hfail || ctx->hfail[0] == 0) return WF_OK;
+  return fail(ctx, WF_ERR_COMM,
+              "a peer did not signal within " + std::to_string(ctx->timeout_ns / 1000000000.0) +
+                  " s (waited for count " + std::to_string(ctx->hfail[1]) + ", saw " + std::to_string(ctx->hfail[2]) +
+                  "); finalize the context");
+}
+
+// begin a collective call: the failure check and the call sequence number (wf_qkv_proj's
+// fused gather is consumed only by the call right after it)
+wf_status begin_call(wf_ctx* ctx) {
+  ++ctx->seq;
+  return comm_ok(ctx);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -1382,20 +1405,30 @@ wf_status wf_get_uid(wf_uid* out) {
   return WF_OK;
 }
 
-wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, wf_ctx** out) {
+// Shared part of wf_init / wf_init_bootstrap: context, plan, streams.
+static wf_status init_real(int P, int C, wf_topology topo, int rank, wf_ctx** out) {
   if (!out) return fail(nullptr, WF_ERR_ARG, "wf_init: null out");
   if (topo != WF_TOPO_COLLECT_INTRA && topo != WF_TOPO_P2P_INTRA) return fail(nullptr, WF_ERR_CONFIG, "bad topology");
   if (rank < 0 || rank >= P) return fail(nullptr, WF_ERR_CONFIG, "rank out of range");
+  if (P > kMaxRanks) return fail(nullptr, WF_ERR_CONFIG, "P > 64 ranks is not supported by this build");
   wf_ctx* ctx = nullptr;
   wf_ctx* tmp = nullptr;
   WCK(new_ctx(P, C, &ctx, &tmp));
   ctx->rank = rank;
+  ctx->ipc = P > 1;  // peer-memory transport between the P ranks
   wf_status s = make_streams(ctx);
   if (s != WF_OK) {
     g_ctxless_err = ctx->err;
     wf_finalize(ctx);
     return s;
   }
+  *out = ctx;
+  return WF_OK;
+}
+
+wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, wf_ctx** out) {
+  wf_ctx* ctx = nullptr;
+  WCK(init_real(P, C, topo, rank, &ctx));
   if (P > 1) {
     if (!uid) {
       wf_finalize(ctx);
@@ -1408,12 +1441,18 @@ wf_status wf_init(int P, int C, wf_topology topo, int rank, const wf_uid* uid, w
       wf_finalize(ctx);
       return fail(nullptr, WF_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
-    // transport: peer-memory copies + flags (default) or NCCL send/recv (WF_TRANSPORT=nccl)
-    const char* tp = std::getenv("WF_TRANSPORT");
-    ctx->ipc = !(tp && std::string(tp) == "nccl") && P <= kMaxRanks;
-    const char* du = std::getenv("WF_DIRECT_UNITPIPE");
-    ctx->direct_unitpipe = du && du[0] == '1';
   }
+  *out = ctx;
+  return WF_OK;
+}
+
+wf_status wf_init_bootstrap(int P, int C, wf_topology topo, int rank, wf_allgather_fn allgather, void* user,
+                            wf_ctx** out) {
+  if (P > 1 && !allgather) return fail(nullptr, WF_ERR_ARG, "wf_init_bootstrap: allgather required when P > 1");
+  wf_ctx* ctx = nullptr;
+  WCK(init_real(P, C, topo, rank, &ctx));
+  ctx->ag_fn = allgather;
+  ctx->ag_user = user;
   *out = ctx;
   return WF_OK;
 }
@@ -1424,10 +1463,6 @@ wf_status wf_init_emulated(int P, int C, wf_ctx** out) {
   wf_ctx* tmp = nullptr;
   WCK(new_ctx(P, C, &ctx, &tmp));
   ctx->emulated = true;
-  const char* up = std::getenv("WF_EMU_UNITPIPE");
-  ctx->emu_unitpipe = up && up[0] == '1';
-  const char* du = std::getenv("WF_DIRECT_UNITPIPE");
-  ctx->direct_unitpipe = du && du[0] == '1';
   wf_status s = make_streams(ctx);
   if (s != WF_OK) {
     g_ctxless_err = ctx->err;
@@ -1438,12 +1473,20 @@ wf_status wf_init_emulated(int P, int C, wf_ctx** out) {
   return WF_OK;
 }
 
+wf_status wf_set_timeout(wf_ctx* ctx, double seconds) {
+  if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
+  if (!(seconds > 0)) return fail(ctx, WF_ERR_ARG, "wf_set_timeout: seconds must be > 0");
+  ctx->timeout_ns = static_cast<uint64_t>(seconds * 1e9);
+  return WF_OK;
+}
+
 wf_status wf_attn_fwd(wf_ctx* ctx, const void* Q, const void* K, const void* V, int64_t N, int heads, int head_dim,
                       int causal, void* O, float* LSE, void* stream) {
   if (!ctx) return fail(nullptr, WF_ERR_ARG, "null ctx");
   if (!Q || !K || !V || !O || !LSE) return fail(ctx, WF_ERR_ARG, "wf_attn_fwd: null pointer");
   if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
     return fail(ctx, WF_ERR_ARG, "wf_attn_fwd: pointers must be 16-byte aligned");
+  WCK(begin_call(ctx));
   Geo g;
   WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
   WCK(ensure_ws(ctx, g));
@@ -1457,6 +1500,7 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
   if (!X || !W || !Q || !K || !V) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: null pointer");
   for (const void* p : {X, W, static_cast<const void*>(Q), static_cast<const void*>(K), static_cast<const void*>(V)})
     if (!aligned16(p)) return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: pointers must be 16-byte aligned");
+  WCK(begin_call(ctx));
   Geo g;
   WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
   const int64_t n = g.n, E = g.E;
@@ -1475,8 +1519,8 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
   if (!make_tmap_2d(&tw, W, 3 * E, hidden, pair ? 128 : bn))
     return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
   // fused gather: the epilogue writes straight into the team buffers (peer memory or, emulated,
-  // the virtual ranks' workspaces); the NCCL transport keeps the separate gather.
-  bool fuse = C > 1 && (ctx->emulated || ctx->ipc) && !(ctx->debug & WF_DEBUG_NO_TRANSFER);
+  // the virtual ranks' workspaces)
+  bool fuse = C > 1 && !(ctx->debug & WF_DEBUG_NO_TRANSFER);
   if (fuse && C + 2 > WF_GEMM_MAX_DST) fuse = false;
   if (fuse && ctx->ipc) WCK(ipc_barrier(ctx, st));  // every peer is done with its team buffers
   auto lp = [&](int r, bf16* p) { return addressable(ctx, r) ? p : nullptr; };
@@ -1528,6 +1572,7 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
     WCK(kcheck(ctx, pair ? launch_gemm_pair(tx, tw, ga, st) : launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
   }
   if (fuse) {
+    ctx->proj_seq = ctx->seq;
     ctx->proj_q = Q;
     ctx->proj_k = K;
     ctx->proj_v = V;
@@ -1545,6 +1590,7 @@ wf_status wf_attn_bwd(wf_ctx* ctx, const void* dO, const void* Q, const void* K,
   for (const void* p : {dO, Q, K, V, O, static_cast<const void*>(LSE), static_cast<const void*>(dQ),
                         static_cast<const void*>(dK), static_cast<const void*>(dV)})
     if (!aligned16(p)) return fail(ctx, WF_ERR_ARG, "wf_attn_bwd: pointers must be 16-byte aligned");
+  WCK(begin_call(ctx));
   Geo g;
   WCK(check_shape(ctx, N, heads, head_dim, causal, &g));
   WCK(ensure_ws(ctx, g));
@@ -1584,7 +1630,7 @@ wf_status wf_workspace_bytes(int P, int C, int64_t N, int heads, int head_dim, i
   if (s != WF_OK) return fail(nullptr, s, ctx->err);
   RankBufs b{};
   CarveList items;
-  carve_rank(g, b, items);
+  carve_rank(g, b, items, false);  // real mode (peer memory) carve
   *bytes = carve_total(items);
   return WF_OK;
 }
@@ -1619,7 +1665,7 @@ wf_status wf_set_schedule(wf_ctx* ctx, int sched) {
   if (sched != WF_SCHED_GATHER_SHUFFLE && sched != WF_SCHED_DIRECT_PULL)
     return fail(ctx, WF_ERR_CONFIG, "wf_set_schedule: unknown schedule");
   ctx->sched = sched;
-  ctx->proj_q = ctx->proj_k = ctx->proj_v = nullptr;  // a pending fused gather used the old layout
+  ++ctx->seq;  // a pending fused gather used the old layout
   return WF_OK;
 }
 
@@ -1715,9 +1761,9 @@ wf_status wf_finalize(wf_ctx* ctx) {
   if (!ctx) return WF_OK;
   if (ctx->ws) {
     cudaDeviceSynchronize();
-    if (ctx->ipc && ctx->comm_stream && !ctx->peer_base.empty()) {
+    if (ctx->ipc && ctx->comm_stream && !ctx->peer_base.empty() && comm_ok(ctx) == WF_OK) {
       // collective: peers may still pull from this workspace -- free it after every rank
-      // has finished its last call (a rank that never joins makes the wait trap in 30 s)
+      // has finished its last call (a rank that never joins ends the wait at the timeout)
       if (ipc_barrier(ctx, ctx->comm_stream) == WF_OK) cudaStreamSynchronize(ctx->comm_stream);
     }
     for (size_t r = 0; r < ctx->peer_base.size(); ++r)
@@ -1735,6 +1781,7 @@ wf_status wf_finalize(wf_ctx* ctx) {
   for (auto& pr : ctx->ev_bwd) ctx->ev_pool.push_back(pr.first), ctx->ev_pool.push_back(pr.second);
   for (auto& pr : ctx->ev_phase) ctx->ev_pool.push_back(pr.second.first), ctx->ev_pool.push_back(pr.second.second);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->hfail) cudaFreeHost(const_cast<uint32_t*>(ctx->hfail));
   delete ctx;
   return WF_OK;
 }

@@ -7,7 +7,7 @@
 // A sender's stream writes a flag with st.release.sys after its copy-engine copies (stream
 // order: the copies have completed); the receiver's stream spins in a one-warp kernel with
 // ld.acquire.sys until the count is reached, so the kernels after it see the data.  Counts
-// only grow, so flags never need resetting.
+// only grow, so flags never need resetting.  A timed-out wait is reported, not trapped.
 #include <cstdint>
 
 #include "common.h"
@@ -31,7 +31,16 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Thread i: (optionally) publish sig.val[i] at sig.dst[i], then wait until *wait.flag[i] >= wait.val[i].
+// A wait that outlives wait.timeout_ns (a peer is gone or stalled) records the failure in
+// the context's host-mapped words and returns: the library reports WF_ERR_COMM on the next
+// call instead of poisoning the CUDA context with a trap.  Later waits return at once.
 __global__ void wf_signal_wait_kernel(SigArgs sig, SigArgs wait) {
   const int i = threadIdx.x;
   if (i < sig.n) {
@@ -39,12 +48,22 @@ __global__ void wf_signal_wait_kernel(SigArgs sig, SigArgs wait) {
     st_release_sys(sig.dst[i], sig.val[i]);
   }
   if (i < wait.n) {
+    if (wait.fail && ld_volatile(wait.fail) != 0) return;
     const uint64_t t0 = gtimer();
     uint32_t spins = 0;
-    while (static_cast<int32_t>(ld_acquire_sys(wait.dst[i]) - wait.val[i]) < 0) {
+    uint32_t seen;
+    while (static_cast<int32_t>((seen = ld_acquire_sys(wait.dst[i])) - wait.val[i]) < 0) {
       if ((++spins & 255u) == 0) {
         __nanosleep(200);
-        if (gtimer() - t0 > 30000000000ull) __trap();  // 30 s: a peer is gone; fail loudly
+        if (gtimer() - t0 > wait.timeout_ns) {
+          if (wait.fail) {
+            wait.fail[1] = wait.val[i];
+            wait.fail[2] = seen;
+            __threadfence_system();
+            atomicExch_system(wait.fail, 1u);
+          }
+          return;
+        }
       }
     }
   }

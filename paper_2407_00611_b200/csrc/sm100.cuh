@@ -307,8 +307,8 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 // Two exponentials on the FMA pipe with packed fp32x2 arithmetic (same polynomial as
 // poly_exp2): 6 FP32x2 + 4 integer instructions for the pair, no MUFU.
 __device__ __forceinline__ float2 poly_exp2x2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -125.f);  // keeps the exponent field of p * 2^n positive
+  x.y = fmaxf(x.y, -125.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);
   const float2 t = fadd2(x, magic);
   const float2 f = fadd2(x, fadd2(magic, make_float2(-t.x, -t.y)));

@@ -48,39 +48,64 @@ def label(C, sched):
     return f"{C}" + ("/direct" if sched else "")
 
 
-def search(P, rank, N, heads, head_dim, causal, steps=2, warmup=1, cands=None, group=None):
-    """Profile each candidate (C, schedule); returns (best_C, best_schedule, {label: ms_per_step})."""
+def search(P, rank, N, heads, head_dim, causal, steps=5, warmup=2, rounds=3, cands=None, group=None,
+           emulated=False):
+    """Profile each candidate (C, schedule); returns (best_C, best_schedule, table) with
+    table[label] = {"ms": median over rounds of the per-step time (max over ranks),
+    "spread": (max - min) / median over the rounds}.
+
+    Every candidate gets its own context (kept alive for the whole search) and `warmup`
+    untimed steps; then `rounds` interleaved rounds time `steps` steps of every candidate
+    in turn, so slow drifts of the clock (power cap) hit all candidates alike.  emulated:
+    all P ranks on this GPU (wf_init_emulated; tests), inputs stacked rank-major."""
+    import statistics
     import torch.distributed as dist
     dev = torch.device("cuda", torch.cuda.current_device())
-    n = N // P
+    dist_on = P > 1 and not emulated
+    rows = N if emulated else N // P
     g = torch.Generator(device=dev).manual_seed(777 + rank)
-    q, k, v, do = (torch.randn((n, heads, head_dim), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
+    q, k, v, do = (torch.randn((rows, heads, head_dim), generator=g, device=dev).to(torch.bfloat16) for _ in range(4))
     o = torch.empty_like(q)
-    lse = torch.empty((heads, n), dtype=torch.float32, device=dev)
+    lse = torch.empty((P, heads, rows // P) if emulated else (heads, rows), dtype=torch.float32, device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    table, keys = {}, {}
-    for C, sched in cands or variants(P):
-        ctx = Context(P, C, rank=rank, group=group)
-        if sched:
-            ctx.set_schedule(sched)
-        for _ in range(warmup):
-            ctx.fwd(q, k, v, N, causal, o=o, lse=lse)
-            ctx.bwd(do, q, k, v, o, lse, N, causal, dq=dq, dk=dk, dv=dv)
-        if P > 1:
-            dist.barrier(group=group)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            ctx.fwd(q, k, v, N, causal, o=o, lse=lse)
-            ctx.bwd(do, q, k, v, o, lse, N, causal, dq=dq, dk=dk, dv=dv)
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
-        if P > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        table[label(C, sched)] = float(t.item())
-        keys[label(C, sched)] = (C, sched)
-        ctx.close()
-    best = min(table, key=table.get)
-    return keys[best][0], keys[best][1], table
+    cands = list(cands or variants(P))
+    ctxs = []
+    try:
+        for C, sched in cands:
+            ctx = Context(P, C, rank=rank, group=group, emulated=emulated)
+            ctxs.append(ctx)
+            if sched:
+                ctx.set_schedule(sched)
+
+        def run(ctx, n):
+            for _ in range(n):
+                ctx.fwd(q, k, v, N, causal, o=o, lse=lse)
+                ctx.bwd(do, q, k, v, o, lse, N, causal, dq=dq, dk=dk, dv=dv)
+
+        for ctx in ctxs:
+            run(ctx, warmup)
+        times = {label(C, s): [] for C, s in cands}
+        for _ in range(rounds):
+            for (C, sched), ctx in zip(cands, ctxs):
+                if dist_on:
+                    dist.barrier(group=group)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run(ctx, steps)
+                e1.record()
+                torch.cuda.synchronize()
+                t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+                if dist_on:
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                times[label(C, sched)].append(float(t.item()))
+    finally:
+        for ctx in ctxs:
+            ctx.close()
+    table = {}
+    for key, ts in times.items():
+        med = statistics.median(ts)
+        table[key] = {"ms": med, "spread": (max(ts) - min(ts)) / med}
+    best = min(table, key=lambda x: table[x]["ms"])
+    C, sched = dict((label(c, s), (c, s)) for c, s in cands)[best]
+    return C, sched, table

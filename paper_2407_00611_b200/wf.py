@@ -10,7 +10,7 @@ import ctypes
 
 import torch
 
-from ._lib import KINDS, WfEvent, WfUid, lib
+from ._lib import ALLGATHER_FN, KINDS, WfEvent, WfUid, lib
 
 __all__ = ["WFError", "block_fwd", "block_bwd", "Context", "plan", "plan_trace", "shard_ranges"]
 
@@ -42,6 +42,11 @@ def _i32arr(xs):
         return None, 0
     arr = (ctypes.c_int32 * len(xs))(*[int(x) for x in xs])
     return arr, len(xs)
+
+
+def _backend(group):
+    import torch.distributed as dist
+    return dist.get_backend(group)
 
 
 def _bf16(t, name):
@@ -77,37 +82,38 @@ def gemm_bf16(a, b, y=None, a_mn=False, b_mn=False):
     return y
 
 
-def rmsnorm_fwd(x, w, eps=1e-5, y=None, rstd=None):
-    """y = x rstd w (wf_rmsnorm_fwd); returns (y, rstd fp32 [rows])."""
+def layernorm_fwd(x, w, b, eps=1e-5, y=None):
+    """y = (x - mean) rstd w + b (wf_layernorm_fwd); returns (y, mean, rstd) (fp32 [rows])."""
     rows, H = x.shape
     y = torch.empty_like(x) if y is None else y
-    rstd = torch.empty((rows,), dtype=torch.float32, device=x.device) if rstd is None else rstd
-    _check(lib().wf_rmsnorm_fwd(_ptr(_bf16(x, "x")), _ptr(_bf16(w, "w")), rows, H, float(eps), _ptr(y), _ptr(rstd),
-                                _stream()))
-    return y, rstd
+    mean = torch.empty((rows,), dtype=torch.float32, device=x.device)
+    rstd = torch.empty((rows,), dtype=torch.float32, device=x.device)
+    _check(lib().wf_layernorm_fwd(_ptr(_bf16(x, "x")), _ptr(_bf16(w, "w")), _ptr(_bf16(b, "b")), rows, H, float(eps),
+                                  _ptr(_bf16(y, "y")), _ptr(mean), _ptr(rstd), _stream()))
+    return y, mean, rstd
 
 
-def rmsnorm_bwd(dy, x, w, rstd, dw, dres=None, dx=None):
-    """dx (+ dres) and dw += (wf_rmsnorm_bwd); dw fp32 [H] accumulates."""
+def layernorm_bwd(dy, x, w, mean, rstd, dw, db, dres=None, dx=None):
+    """dx (+ dres) and dw, db += (wf_layernorm_bwd); dw, db fp32 [H] accumulate."""
     rows, H = x.shape
     dx = torch.empty_like(x) if dx is None else dx
-    _check(lib().wf_rmsnorm_bwd(_ptr(_bf16(dy, "dy")), _ptr(x), _ptr(w), _ptr(rstd), _ptr(dres), rows, H, _ptr(dx),
-                                _ptr(dw), _stream()))
+    _check(lib().wf_layernorm_bwd(_ptr(_bf16(dy, "dy")), _ptr(_bf16(x, "x")), _ptr(_bf16(w, "w")), _ptr(mean),
+                                  _ptr(rstd), _ptr(dres), rows, H, _ptr(_bf16(dx, "dx")), _ptr(dw), _ptr(db),
+                                  _stream()))
     return dx
 
 
-def swiglu_fwd(gu, h=None):
-    rows, F2 = gu.shape
-    h = torch.empty((rows, F2 // 2), dtype=torch.bfloat16, device=gu.device) if h is None else h
-    _check(lib().wf_swiglu_fwd(_ptr(_bf16(gu, "gu")), rows, F2 // 2, _ptr(h), _stream()))
+def gelu_fwd(u, h=None):
+    h = torch.empty_like(u) if h is None else h
+    _check(lib().wf_gelu_fwd(_ptr(_bf16(u, "u")), u.numel(), _ptr(_bf16(h, "h")), _stream()))
     return h
 
 
-def swiglu_bwd(dh, gu, dgu=None):
-    rows, F2 = gu.shape
-    dgu = torch.empty_like(gu) if dgu is None else dgu
-    _check(lib().wf_swiglu_bwd(_ptr(_bf16(dh, "dh")), _ptr(gu), rows, F2 // 2, _ptr(dgu), _stream()))
-    return dgu
+def gelu_bwd(dh, u, du=None):
+    du = torch.empty_like(u) if du is None else du
+    _check(lib().wf_gelu_bwd(_ptr(_bf16(dh, "dh")), _ptr(_bf16(u, "u")), u.numel(), _ptr(_bf16(du, "du")),
+                             _stream()))
+    return du
 
 
 def add_bf16(a, b, y=None):
@@ -170,14 +176,43 @@ def workspace_bytes(P, C, N, heads, head_dim, causal):
     return int(out.value)
 
 
-class Context:
-    """A wf_ctx: real (one rank of a torch.distributed job) or emulated (all P ranks on one GPU)."""
+def _host_allgather(P, group):
+    """wf_allgather_fn over torch.distributed (the bootstrap of wf_init_bootstrap)."""
+    import torch.distributed as dist
 
-    def __init__(self, P, C, rank=0, emulated=False, group=None, topology=0):
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+    def fn(inp, out, nbytes, user):
+        try:
+            t = torch.frombuffer(bytearray(ctypes.string_at(inp, nbytes)), dtype=torch.uint8).to(dev)
+            outs = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(P)]
+            dist.all_gather(outs, t, group=group)
+            data = torch.cat(outs).cpu().numpy().tobytes()
+            ctypes.memmove(out, data, P * nbytes)
+            return 0
+        except Exception:  # pragma: no cover - reported as WF_ERR_COMM by the library
+            return 1
+
+    return ALLGATHER_FN(fn)
+
+
+class Context:
+    """A wf_ctx: real (one rank of a torch.distributed job) or emulated (all P ranks on one GPU).
+
+    Real mode bootstraps the peer-memory transport through NCCL (wf_init) when the process
+    group is NCCL, and through the group's host all-gather (wf_init_bootstrap) otherwise --
+    e.g. gloo, which lets several ranks share one GPU in tests."""
+
+    def __init__(self, P, C, rank=0, emulated=False, group=None, topology=0, timeout_s=None):
         self.P, self.C, self.rank, self.emulated = P, C, rank, emulated
+        self._ag = None
         h = ctypes.c_void_p()
         if emulated:
             _check(lib().wf_init_emulated(P, C, ctypes.byref(h)))
+        elif P > 1 and _backend(group) != "nccl":
+            self._ag = _host_allgather(P, group)
+            _check(lib().wf_init_bootstrap(P, C, topology, rank, ctypes.cast(self._ag, ctypes.c_void_p), None,
+                                           ctypes.byref(h)))
         else:
             uid = WfUid()
             if P > 1:
@@ -192,12 +227,30 @@ class Context:
                     uid.bytes[i] = b
             _check(lib().wf_init(P, C, topology, rank, ctypes.byref(uid), ctypes.byref(h)))
         self.h = h
+        if timeout_s is not None:
+            _check(lib().wf_set_timeout(self.h, float(timeout_s)), self.h)
+
+    def _check_rows(self, rows, N, what):
+        want = N if self.emulated else N // self.P
+        if N % self.P or rows != want:
+            raise WFError(f"{what}: {rows} rows, expected {want} (N = {N}, P = {self.P}, "
+                          f"{'emulated: all ranks stacked' if self.emulated else 'one rank shard'})")
+
+    def _lse_shape(self, rows, h):
+        return (self.P, h, rows // self.P) if self.emulated else (h, rows)
 
     def fwd(self, q, k, v, N, causal, o=None, lse=None):
         rows, h, d = q.shape
-        o = torch.empty_like(q) if o is None else o
-        lse_shape = (self.P, h, rows // self.P) if self.emulated else (h, rows)
+        self._check_rows(rows, N, "fwd")
+        for t, name in ((q, "q"), (k, "k"), (v, "v")):
+            _bf16(t, name)
+            if t.shape != q.shape:
+                raise WFError(f"fwd: {name} shape {tuple(t.shape)} != q shape {tuple(q.shape)}")
+        o = torch.empty_like(q) if o is None else _bf16(o, "o")
+        lse_shape = self._lse_shape(rows, h)
         lse = torch.empty(lse_shape, dtype=torch.float32, device=q.device) if lse is None else lse
+        if o.shape != q.shape or tuple(lse.shape) != lse_shape or lse.dtype != torch.float32 or not lse.is_contiguous():
+            raise WFError("fwd: o must match q; lse must be contiguous fp32 " + str(lse_shape))
         _check(lib().wf_attn_fwd(self.h, _ptr(q), _ptr(k), _ptr(v), N, h, d, int(causal), _ptr(o), _ptr(lse),
                                  _stream()), self.h)
         return o, lse
@@ -206,6 +259,9 @@ class Context:
         """Alg. 1 l.1 AllGather_QKVmatmul (wf_qkv_proj): x [rows, hidden], w [3 heads head_dim, hidden]
         -> q, k, v [rows, heads, head_dim]; with C > 1 the team gather rides on the GEMM epilogue."""
         rows, hidden = x.shape
+        self._check_rows(rows, N, "qkv_proj")
+        if tuple(w.shape) != (3 * heads * head_dim, hidden):
+            raise WFError(f"qkv_proj: w shape {tuple(w.shape)} != {(3 * heads * head_dim, hidden)}")
         q = torch.empty((rows, heads, head_dim), dtype=torch.bfloat16, device=x.device) if q is None else q
         k = torch.empty_like(q) if k is None else k
         v = torch.empty_like(q) if v is None else v
@@ -215,9 +271,20 @@ class Context:
 
     def bwd(self, do, q, k, v, o, lse, N, causal, dq=None, dk=None, dv=None):
         rows, h, d = q.shape
-        dq = torch.empty_like(q) if dq is None else dq
-        dk = torch.empty_like(k) if dk is None else dk
-        dv = torch.empty_like(v) if dv is None else dv
+        self._check_rows(rows, N, "bwd")
+        for t, name in ((do, "do"), (q, "q"), (k, "k"), (v, "v"), (o, "o")):
+            _bf16(t, name)
+            if t.shape != q.shape:
+                raise WFError(f"bwd: {name} shape {tuple(t.shape)} != q shape {tuple(q.shape)}")
+        lse_shape = self._lse_shape(rows, h)
+        if tuple(lse.shape) != lse_shape or lse.dtype != torch.float32 or not lse.is_contiguous():
+            raise WFError("bwd: lse must be contiguous fp32 " + str(lse_shape))
+        dq = torch.empty_like(q) if dq is None else _bf16(dq, "dq")
+        dk = torch.empty_like(k) if dk is None else _bf16(dk, "dk")
+        dv = torch.empty_like(v) if dv is None else _bf16(dv, "dv")
+        for t, name in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+            if t.shape != q.shape:
+                raise WFError(f"bwd: {name} shape {tuple(t.shape)} != q shape {tuple(q.shape)}")
         _check(lib().wf_attn_bwd(self.h, _ptr(do), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), N, h, d,
                                  int(causal), _ptr(dq), _ptr(dk), _ptr(dv), _stream()), self.h)
         return dq, dk, dv
@@ -259,6 +326,7 @@ class Context:
         if self.h:
             lib().wf_finalize(self.h)
             self.h = None
+        self._ag = None
 
     def __del__(self):
         try:

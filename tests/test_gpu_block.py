@@ -133,10 +133,9 @@ def test_block_bwd(causal, d):
 
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("case", ["contiguous", "zigzag", "state"])
-def test_block_fwd_cta_pair(causal, case, monkeypatch):
-    """The opt-in CTA-pair forward (attn_fwd2.cu, WF_FWD_PAIR=1): query rows in whole pairs of
-    pairs (nq % 512 == 0), contiguous and zigzag chunks, with and without an incoming state."""
-    monkeypatch.setenv("WF_FWD_PAIR", "1")
+def test_block_fwd_chained_blocks(causal, case):
+    """Multi-tile query blocks (nq % 512 == 0), contiguous and zigzag chunks, and a state
+    chained through two K/V blocks (forward_iteration) ending in the bf16 output."""
     wf = _wf()
     h, d = 2, 128
     if case == "contiguous":
@@ -162,20 +161,5 @@ def test_block_fwd_cta_pair(causal, case, monkeypatch):
         o_ref, l_ref = attention_fwd(to_f64(q[:n]), to_f64(torch.cat([b[1] for b in blocks])),
                                      to_f64(torch.cat([b[2] for b in blocks])), qp, kp, causal)
         o, l = to_f64(ob), lse.cpu().double().numpy()
-    eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
-    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
-
-
-@pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("case", ["contiguous", "zigzag"])
-def test_block_fwd_split_rows(causal, case, monkeypatch):
-    """The opt-in split-row forward (attn_fwd3.cu, WF_FWD_SPLIT=1): two softmax threads per
-    query row, partial maxima exchanged through shared memory."""
-    monkeypatch.setenv("WF_FWD_SPLIT", "1")
-    if case == "contiguous":
-        o, l, o_ref, l_ref = _run_fwd(1024, 1024, 2, 128, causal, 1024, [0], [0], peaky=True)
-    else:
-        o, l, o_ref, l_ref = _run_fwd(1024, 1024, 3, 128, causal, 256, [0, 1792, 512, 1280], [256, 1536, 768, 1024],
-                                      peaky=True)
     eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
     assert eo <= O_TOL and el <= LSE_TOL, (eo, el)

@@ -101,10 +101,9 @@ def test_emulated_dit_shape():
 
 @pytest.mark.parametrize("P,C", [(2, 2), (4, 4), (8, 4)])
 @pytest.mark.parametrize("causal", [False, True])
-def test_emulated_unit_pipelined_extension(P, C, causal, monkeypatch):
+def test_emulated_unit_pipelined_extension(P, C, causal):
     # the real-mode decomposition of the extension regime (one launch per (query unit, key
     # unit), W = P / C key units per slice; W = 2 at P = 8, C = 4), run for every virtual rank
-    monkeypatch.setenv("WF_EMU_UNITPIPE", "1")
     N = 256 * P if causal else 128 * P * 2
     h, d = 2, 128
     inputs, outs, trace = run_path(P, C, N, h, d, causal, seed=P + C + 1)
@@ -115,12 +114,8 @@ def test_emulated_unit_pipelined_extension(P, C, causal, monkeypatch):
 
 @pytest.mark.parametrize("P,C", [(4, 2), (8, 2)])
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("unitpipe", ["0", "1"])
-def test_emulated_direct_pull(P, C, causal, unitpipe, monkeypatch):
-    # DIRECT-PULL init (wf_set_schedule, reading c21): values, and the trace of the variant;
-    # at P = 4, C = 2 (R = 1) with WF_EMU_UNITPIPE=1 the unit-pipelined decomposition runs
-    monkeypatch.setenv("WF_EMU_UNITPIPE", unitpipe)
-    monkeypatch.setenv("WF_DIRECT_UNITPIPE", unitpipe)
+def test_emulated_direct_pull(P, C, causal):
+    # DIRECT-PULL init (wf_set_schedule, reading c21): values, and the trace of the variant
     N = 256 * P if causal else 128 * P * 2
     h, d = 2, 128
     inputs, outs, trace = run_path(P, C, N, h, d, causal, seed=P + C + 5, sched=1)

@@ -13,7 +13,6 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("WF_EMU_UNITPIPE", "1")  # the real-mode decomposition of the extension regime
 import paper_2407_00611_b200 as wf  # noqa: E402
 from paper_2407_00611_b200.scheduler import candidates  # noqa: E402
 
