@@ -158,7 +158,6 @@ extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, i
   a.o_out_bf16 = static_cast<__nv_bfloat16*>(o_bf16);
   a.lse_out = lse_out;
   a.lse_blk = nq;
-  a.kbase = k;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_rows(&tq, q, nq, heads, head_dim) || !make_tmap_rows(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim) ||
       !make_tmap_rows(&tv, v, nk > 0 ? nk : WF_TILE, heads, head_dim))

@@ -108,7 +108,6 @@ struct FwdArgs {
   int lse_blk;                    // lse layout: rows in blocks of lse_blk, [nq/blk][heads][blk]
   unsigned long long* tl;         // debug timeline (null = off), see wf_debug_timeline
   int tl_cta;
-  const void* kbase;              // K rows (for the CTA-pair kernel's 64-row key boxes; may be null)
 };
 
 // Arguments of one block-backward launch (flash-attention backward):

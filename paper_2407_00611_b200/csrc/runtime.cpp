@@ -743,7 +743,6 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         fa.o_out_f32 = b.o_state + jm * n * E;
         fa.lse_out = b.lse_state + jm * h * n;
         fa.lse_blk = g.n;
-        fa.kbase = kp;
         CUtensorMap tq, tk, tv;
         if (!make_tmap_rows(&tq, qp, fa.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, fa.nk, g.h, g.d) ||
             !make_tmap_rows(&tv, vp, fa.nk, g.h, g.d))
@@ -857,7 +856,6 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         a.lse_out = b.lse_state;
       }
       if (ctx->dry) return WF_OK;
-      a.kbase = slot_k(r, s);
       CUtensorMap tq, tk, tv;
       if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
           !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))

@@ -108,7 +108,7 @@ def _job_attn(wf, rank, world, C, N, causal, repeat=1):
     torch.cuda.synchronize()
     tr = ctx.trace()
     ctx.close()
-    first = [x.cpu() for x in outs[0]]
+    first = [x.float().cpu().numpy() for x in outs[0]]  # numpy: no shared-memory tensors across processes
     same_o = all(torch.equal(x[0], outs[0][0]) and torch.equal(x[1], outs[0][1]) for x in outs)
     g0 = torch.cat([x.float().flatten() for x in outs[0][2:]])
     gdev = max(float((torch.cat([y.float().flatten() for y in x[2:]]) - g0).abs().max()) for x in outs)
@@ -229,7 +229,7 @@ def _check_attn(world, C, N, causal, per_rank):
     trace = []
     for r, (res, tr, same_o, gdev) in enumerate(per_rank):
         pos = unit_positions(r, world, N, causal)
-        o, lse, dq, dk, dv = (x.double().numpy() for x in res)
+        o, lse, dq, dk, dv = (np.asarray(x, dtype=np.float64) for x in res)
         assert np.abs(o - o_r[pos]).max() <= 2e-2, (C, causal, r)
         assert np.abs(lse - l_r[:, pos]).max() <= 1e-2, (C, causal, r)
         for g, ref in ((dq, dq_r), (dk, dk_r), (dv, dv_r)):
