@@ -113,6 +113,8 @@ struct wf_ctx {
   volatile uint32_t* hfail = nullptr;
   uint32_t* dfail = nullptr;
   uint64_t timeout_ns = 30000000000ull;
+  // WF_DEBUG_CHECKS builds: the memory ranges a call may touch (caller tensors + workspaces)
+  std::vector<std::pair<const char*, size_t>> dbg_ranges;
   // peer-memory transport (real mode, P > 1): CUDA IPC mapped workspaces + flag signalling
   bool ipc = false;
   std::vector<char*> peer_base;
@@ -399,6 +401,8 @@ bool addressable(const wf_ctx* ctx, int r) { return local(ctx, r) || (ctx->ipc &
 
 cudaEvent_t pool_event(wf_ctx* ctx);
 cudaEvent_t prof_begin(wf_ctx* ctx, cudaStream_t st);
+wf_status dbg_check_segs(wf_ctx* ctx, const std::vector<Xfer>& xs);
+wf_status dbg_check(wf_ctx* ctx, const void* p, int64_t bytes, const char* what);
 
 // Launch a signal/wait kernel whose waits report a timeout through the context's
 // host-mapped failure words (WF_ERR_COMM on the next call) instead of trapping.
@@ -424,6 +428,7 @@ wf_status run_phase(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<wf_event>& t
     }
   }
   if (ctx->dry) return WF_OK;
+  if (part != kPhaseWait) WCK(dbg_check_segs(ctx, xs));
   if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
   if (ctx->emulated) {
     if (part == kPhaseWait) return WF_OK;
@@ -478,6 +483,7 @@ wf_status run_phase_per_source(wf_ctx* ctx, std::vector<Xfer>& xs, std::vector<w
     for (const Seg& sg : x.segs) bytes += sg.bytes;
     trace.push_back(wf_event{x.pass, x.kind, x.step, x.src, x.dst, x.block, bytes});
   }
+  WCK(dbg_check_segs(ctx, xs));
   if (ctx->debug & WF_DEBUG_NO_TRANSFER) return WF_OK;
   const int ch = st == ctx->comm_stream ? 1 : 0;
   cudaEvent_t pe0 = xs.empty() ? nullptr : prof_begin(ctx, st);
@@ -553,6 +559,82 @@ wf_status kcheck(wf_ctx* ctx, cudaError_t e, const char* what) {
   return WF_OK;
 }
 
+// ------------------------------------------------------------------ debug bounds checks
+// A WF_DEBUG_CHECKS build (compute-sanitizer is not available on this pool) verifies that
+// every copy segment, partial and accumulator pointer the schedule hands to a copy engine
+// or a kernel lies inside one of the ranges the call may touch: the caller's tensors of
+// this call, this rank's workspace, or a peer's mapped workspace.
+void dbg_begin(wf_ctx* ctx, std::initializer_list<std::pair<const void*, size_t>> tensors) {
+#ifdef WF_DEBUG_CHECKS
+  ctx->dbg_ranges.clear();
+  for (auto& t : tensors)
+    if (t.first) ctx->dbg_ranges.push_back({static_cast<const char*>(t.first), t.second});
+  if (ctx->ws) ctx->dbg_ranges.push_back({static_cast<const char*>(ctx->ws), ctx->ws_bytes});
+  for (size_t r = 0; r < ctx->peer_base.size(); ++r)
+    if (ctx->peer_base[r]) ctx->dbg_ranges.push_back({ctx->peer_base[r], ctx->ws_bytes});
+#else
+  (void)ctx;
+  (void)tensors;
+#endif
+}
+wf_status dbg_check(wf_ctx* ctx, const void* p, int64_t bytes, const char* what) {
+#ifdef WF_DEBUG_CHECKS
+  if (!p || bytes <= 0 || ctx->dry) return WF_OK;
+  const char* c = static_cast<const char*>(p);
+  for (auto& r : ctx->dbg_ranges)
+    if (c >= r.first && c + bytes <= r.first + r.second) return WF_OK;
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "debug check: %s [%p, +%lld) outside every tensor / workspace of this call", what,
+                p, static_cast<long long>(bytes));
+  return fail(ctx, WF_ERR_ARG, buf);
+#else
+  (void)ctx;
+  (void)p;
+  (void)bytes;
+  (void)what;
+  return WF_OK;
+#endif
+}
+// operands of one block-forward / block-backward launch
+wf_status dbg_fwd(wf_ctx* ctx, const FwdArgs& a, const void* q, const void* k, const void* v, int64_t E) {
+  WCK(dbg_check(ctx, q, a.nq * E * 2, "block-fwd Q"));
+  WCK(dbg_check(ctx, k, a.nk * E * 2, "block-fwd K"));
+  WCK(dbg_check(ctx, v, a.nk * E * 2, "block-fwd V"));
+  WCK(dbg_check(ctx, a.o_in, a.nq * E * 4, "block-fwd O state in"));
+  WCK(dbg_check(ctx, a.lse_in, static_cast<int64_t>(a.heads) * a.nq * 4, "block-fwd lse in"));
+  WCK(dbg_check(ctx, a.o_out_f32, a.nq * E * 4, "block-fwd O state out"));
+  WCK(dbg_check(ctx, a.o_out_bf16, a.nq * E * 2, "block-fwd O out"));
+  return dbg_check(ctx, a.lse_out, static_cast<int64_t>(a.heads) * a.nq * 4, "block-fwd lse out");
+}
+wf_status dbg_bwd(wf_ctx* ctx, const BwdArgs& a, const void* q, const void* k, const void* v, const void* dO,
+                  int64_t E) {
+  WCK(dbg_check(ctx, q, a.nq * E * 2, "block-bwd Q"));
+  WCK(dbg_check(ctx, dO, a.nq * E * 2, "block-bwd dO"));
+  WCK(dbg_check(ctx, k, a.nk * E * 2, "block-bwd K"));
+  WCK(dbg_check(ctx, v, a.nk * E * 2, "block-bwd V"));
+  WCK(dbg_check(ctx, a.lse, static_cast<int64_t>(a.heads) * a.nq * 4, "block-bwd LSE"));
+  WCK(dbg_check(ctx, a.dsum, static_cast<int64_t>(a.heads) * a.nq * 4, "block-bwd D"));
+  WCK(dbg_check(ctx, a.dq_acc, a.nq * E * 4, "block-bwd dQ accumulator"));
+  WCK(dbg_check(ctx, a.dk_acc, a.nk * E * 4, "block-bwd dK accumulator"));
+  WCK(dbg_check(ctx, a.dv_acc, a.nk * E * 4, "block-bwd dV accumulator"));
+  WCK(dbg_check(ctx, a.dk_out, a.nk * E * 2, "block-bwd dK out"));
+  return dbg_check(ctx, a.dv_out, a.nk * E * 2, "block-bwd dV out");
+}
+wf_status dbg_check_segs(wf_ctx* ctx, const std::vector<Xfer>& xs) {
+#ifdef WF_DEBUG_CHECKS
+  for (const Xfer& x : xs)
+    for (const Seg& sg : x.segs) {
+      if (!local(ctx, x.src) && !ctx->ipc) continue;
+      WCK(dbg_check(ctx, sg.src, sg.bytes, "segment source"));
+      WCK(dbg_check(ctx, sg.dst, sg.bytes, "segment destination"));
+    }
+#else
+  (void)ctx;
+  (void)xs;
+#endif
+  return WF_OK;
+}
+
 // ------------------------------------------------------------------ peer-memory sync helpers
 // Per-call barrier of all ranks: no peer writes into my workspace before I have finished
 // reading what the previous call left there (stream order puts this after my previous work).
@@ -623,6 +705,10 @@ bool last_unit_of(int C, int i, int j) { return (j + 1) % C == i; }
 // push a finished partial into its owner's slot: a copy-engine copy on the comm stream after
 // the producing kernel (peer memory), or a device copy in stream order (emulated)
 wf_status push_segs(wf_ctx* ctx, const Seg* segs, int nseg, cudaStream_t st) {
+  for (int i = 0; i < nseg; ++i) {
+    WCK(dbg_check(ctx, segs[i].src, segs[i].bytes, "pushed partial source"));
+    WCK(dbg_check(ctx, segs[i].dst, segs[i].bytes, "pushed partial destination"));
+  }
   if (ctx->ipc) {
     CK(cudaEventRecord(ctx->ev_b, st));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_b, 0));
@@ -660,6 +746,11 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
   auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_fwd;
   tr.clear();
+  {
+    const int64_t nr = ctx->emulated ? P : 1;
+    dbg_begin(ctx, {{Q, nr * n * E * 2}, {K, nr * n * E * 2}, {V, nr * n * E * 2}, {O, nr * n * E * 2},
+                    {LSE, nr * n * h * 4}});
+  }
   // gathers already delivered by wf_qkv_proj's epilogue (same tensors, same geometry)
   const int64_t key[4] = {g.N, g.h, g.d, g.causal};
   const bool pre = ctx->proj_q && ctx->proj_seq + 1 == ctx->seq && ctx->proj_q == Q && ctx->proj_k == K &&
@@ -747,6 +838,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         if (!make_tmap_rows(&tq, qp, fa.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, fa.nk, g.h, g.d) ||
             !make_tmap_rows(&tv, vp, fa.nk, g.h, g.d))
           return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        WCK(dbg_fwd(ctx, fa, qp, kp, vp, E));
         cudaEvent_t e0 = prof_begin(ctx, st);
         WCK(kcheck(ctx, launch_block_fwd(tq, tk, tv, fa, g.d, st), "block_fwd"));
         prof_end(ctx, st, e0, ctx->ev_fwd);
@@ -860,6 +952,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
           !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
         return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+      WCK(dbg_fwd(ctx, a, qteam(r), slot_k(r, s), slot_v(r, s), E));
       cudaEvent_t e0 = prof_begin(ctx, st);
       wf_status ks = kcheck(ctx, launch_block_fwd(tq, tk, tv, a, g.d, st), "block_fwd");
       prof_end(ctx, st, e0, ctx->ev_fwd);
@@ -953,6 +1046,10 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       }
       m.out = Oout(r);
       m.lse_out = Lout(r);
+      for (int i = 0; i < C; ++i) {
+        WCK(dbg_check(ctx, m.o[i], n * E * 4, "merge partial"));
+        WCK(dbg_check(ctx, m.lse[i], h * n * 4, "merge lse partial"));
+      }
       if (!ctx->dry) WCK(kcheck(ctx, launch_merge(m, st), "merge"));
     }
   }
@@ -970,6 +1067,12 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   auto lp = [&](int r, auto* p) { return addressable(ctx, r) ? p : decltype(p)(nullptr); };
   auto& tr = ctx->trace_bwd;
   tr.clear();
+  {
+    const int64_t nr = ctx->emulated ? P : 1;
+    dbg_begin(ctx, {{dO, nr * n * E * 2}, {Q, nr * n * E * 2}, {K, nr * n * E * 2}, {V, nr * n * E * 2},
+                    {O, nr * n * E * 2}, {LSE, nr * n * h * 4}, {dQ, nr * n * E * 2}, {dK, nr * n * E * 2},
+                    {dV, nr * n * E * 2}});
+  }
   const bool nt = (ctx->debug & WF_DEBUG_NO_TRANSFER) != 0;
   WCK(ipc_barrier(ctx, st));
 
@@ -1077,6 +1180,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         if (!make_tmap_rows(&tq, qp, ba.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, ba.nk, g.h, g.d) ||
             !make_tmap_rows(&tv, vp, ba.nk, g.h, g.d) || !make_tmap_rows(&tdo, dop, ba.nq, g.h, g.d))
           return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        WCK(dbg_bwd(ctx, ba, qp, kp, vp, dop, E));
         cudaEvent_t e0 = prof_begin(ctx, st);
         WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, ba, g.d, st), "block_bwd"));
         prof_end(ctx, st, e0, ctx->ev_bwd);
@@ -1200,6 +1304,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         if (!make_tmap_rows(&tq, pq(r, s), a.nq, g.h, g.d) || !make_tmap_rows(&tk, sk[r], a.nk, g.h, g.d) ||
             !make_tmap_rows(&tv, sv[r], a.nk, g.h, g.d) || !make_tmap_rows(&tdo, pdo(r, s), a.nq, g.h, g.d))
           return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
+        WCK(dbg_bwd(ctx, a, pq(r, s), sk[r], sv[r], pdo(r, s), E));
         cudaEvent_t e0 = prof_begin(ctx, st);
         WCK(kcheck(ctx, launch_block_bwd(tq, tk, tv, tdo, a, g.d, st), "block_bwd"));
         prof_end(ctx, st, e0, ctx->ev_bwd);
@@ -1330,7 +1435,10 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
       SumArgs s{};
       s.n = n * E;
       s.nparts = static_cast<int>(parts[i]->size());
-      for (int k = 0; k < s.nparts; ++k) s.parts[k] = (*parts[i])[k];
+      for (int k = 0; k < s.nparts; ++k) {
+        s.parts[k] = (*parts[i])[k];
+        WCK(dbg_check(ctx, s.parts[k], n * E * 4, "sum partial"));
+      }
       s.out = outs[i];
       WCK(kcheck(ctx, launch_sum(s, st), "sum"));
     }
@@ -1522,6 +1630,11 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
   if (fuse && C + 2 > WF_GEMM_MAX_DST) fuse = false;
   if (fuse && ctx->ipc) WCK(ipc_barrier(ctx, st));  // every peer is done with its team buffers
   auto lp = [&](int r, bf16* p) { return addressable(ctx, r) ? p : nullptr; };
+  {
+    const int64_t nr = ctx->emulated ? P : 1;
+    dbg_begin(ctx, {{X, nr * n * hidden * 2}, {W, 3 * E * hidden * 2}, {Q, nr * n * E * 2}, {K, nr * n * E * 2},
+                    {V, nr * n * E * 2}});
+  }
   for (int r = 0; r < P; ++r) {
     if (!local(ctx, r)) continue;
     const int64_t ro = ctx->emulated ? r : 0;
@@ -1564,6 +1677,8 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
       }
       if (!ok) return fail(ctx, WF_ERR_CONFIG, "wf_qkv_proj: too many gather destinations");
     }
+    for (int part = 0; part < 3; ++part)
+      for (int i = 0; i < ga.ndst[part]; ++i) WCK(dbg_check(ctx, ga.out[part][i], n * E * 2, "projection output"));
     CUtensorMap tx;
     if (!make_tmap_2d(&tx, static_cast<const bf16*>(X) + ro * n * hidden, n, hidden, 128))
       return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
