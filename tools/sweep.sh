@@ -26,7 +26,8 @@ for line in open(p):
     d = json.loads(line)
     if "failed" in d:
         print("FAILED", d["failed"]); continue
-    c = d["config"]; ex = d.get("exposed_comm") or {}
-    print(f"{c['workload'][:38]:38} P={c['P']} C={c['C']} {d['tflops_per_gpu']:7.1f} TF/s/GPU "
-          f"frac {d['frac_of_peak_per_gpu']:.3f} bwd-kernel {d['roofline']['frac']:.3f} exposed {ex.get('frac', 0):.3f}")
+    c, pa = d["config"], d["parallel"]; ex = d.get("exposed_comm") or {}
+    print(f"{c['workload'][:38]:38} P={pa['P']} C={pa['C']} {d['tflops_per_gpu']:7.1f} TF/s/GPU "
+          f"frac(burst) {d['frac_of_peak_per_gpu']['burst']:.3f} bwd-kernel {d['roofline']['frac']:.3f} "
+          f"exposed {ex.get('frac', 0):.3f}")
 PY
