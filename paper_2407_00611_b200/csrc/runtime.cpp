@@ -1477,6 +1477,11 @@ wf_status make_streams(wf_ctx* ctx) {
 // WF_ERR_COMM once a wait of an earlier call timed out (a peer stopped signalling): the
 // failure is sticky, the context must be finalized.
 wf_status comm_ok(wf_ctx* ctx) {
+  if (ctx->comm) {  // the bootstrap communicator (wf_init): an asynchronous NCCL failure
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(ctx->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+      return fail(ctx, WF_ERR_COMM, std::string("bootstrap communicator: ") + ncclGetErrorString(ar));
+  }
   if (!ctx->hfail || ctx->hfail[0] == 0) return WF_OK;
   return fail(ctx, WF_ERR_COMM,
               "a peer did not signal within " + std::to_string(ctx->timeout_ns / 1000000000.0) +
