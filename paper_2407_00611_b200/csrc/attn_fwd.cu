@@ -25,9 +25,21 @@ using namespace sm100;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
-#ifndef WF_POLY_EVERY
-#define WF_POLY_EVERY 0  // every k-th exponential pair on the FMA pipe (0 = all on MUFU); 4 saves 1.5 % (GPT) / 3.6 % (DiT) of fwd time but pushed one peaky parity case past the 2e-2 O bound (0.023): off
+#ifndef WF_FWD_FASTMAX
+#define WF_FWD_FASTMAX 1  // 1: skip the row-max pass while the running max stays valid (see tile())
 #endif
+// Every k-th exponential pair on the FMA pipe (0 = all on MUFU).  Measured with the fast
+// path of tile() (profiles/r02_fwd_experiments.md): at head_dim 72 the forward is bound by
+// the exponentials (MUFU) and 1/4 on the FMA pipe saves 4 % of its time; at head_dim 128 it
+// costs 2 %.  WF_POLY_EVERY overrides the per-head-dim default for experiments.
+template <int D>
+__host__ __device__ constexpr int poly_every() {
+#ifdef WF_POLY_EVERY
+  return WF_POLY_EVERY;
+#else
+  return D < 128 ? 4 : 0;
+#endif
+}
 constexpr float kLn2 = 0.6931471805599453f;
 
 template <int D>
@@ -285,61 +297,80 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int c = 0; c < 128; ++c) s[c] = c > lim ? -INFINITY : s[c];
         }
-        // row max as 8 independent chains (3-input FMNMX), then a small tree: a single
-        // 128-long dependent chain would cost ~500 cycles of latency per tile
-        float mxs[8];
+        // exponentials of the tile against the max mm (log2 domain) -> P (bf16) in TMEM over
+        // S; returns this row's sum of P
+        auto exps = [&](const float mm) -> float {
+          const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mm, -mm);
+          float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(s[k], s[8 + k]);
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[16];
 #pragma unroll
-        for (int c = 16; c < 128; c += 16)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(mxs[k], fmaxf(s[c + k], s[c + 8 + k]));
-        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
-        const float mcand = mx * a.scale_log2;
-        const bool need = mcand > m + 8.0f;
-        if (__any_sync(0xffffffffu, need)) {
-          const float mnew = fmaxf(m, mcand);
-          const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mnew);
-          if (j > 0 || has_state) {
-            // PV_t(j-1) retired with the S_t(j) commit (issued before it)
-#pragma unroll
-            for (int c = 0; c < DP / 16; ++c) {
-              uint32_t r[16];
-              tmem_ld16(tl + cO + c * 16, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tmem_st16(tl + cO + c * 16, r);
+            for (int i = 0; i < 16; ++i) {
+              const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
+              constexpr int PE = poly_every<D>();
+              float2 p;
+              if constexpr (PE > 0) {
+                // masked (-inf) logits exist only on DIAG tiles: those stay on MUFU (exact 0)
+                const bool poly = !DIAG && ((c * 16 + i) % PE) == PE - 1;
+                p = poly ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              } else {
+                p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              }
+              rs2[c] = fadd2(rs2[c], p);
+              pk[i] = pack_bf16x2(p.x, p.y);
             }
+            tmem_st16(tl + cS + c * 16, pk);
           }
-          l *= alpha;
-          m = mnew;
+          const float2 rsa = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+          return rsa.x + rsa.y;
+        };
+        // Fast path (no row-max pass): exponentials against the running max m.  P may then
+        // exceed 1 -- harmless in bf16/fp32 as long as no logit is more than 2^6 above m in
+        // the log2 domain, which the row sum reveals (p <= sum < 2^64).  Otherwise, and on a
+        // row's first visible tile (m = -inf), the slow path takes the row max and applies
+        // the lazy rescale (threshold 2^8) before redoing the exponentials.
+        float rs = 0.f;
+        bool slow = !WF_FWD_FASTMAX || __any_sync(0xffffffffu, m == -INFINITY);
+        if (!slow) {
+          rs = exps(m);
+          slow = __any_sync(0xffffffffu, !(rs < 1.8446744e19f));  // 2^64, also inf / nan
         }
-        tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 3);
-        const float mm = (m == -INFINITY) ? 0.f : m;
-        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mm, -mm);
-        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        if (slow) {
+          // row max as 8 independent chains (3-input FMNMX), then a small tree: a single
+          // 128-long dependent chain would cost ~500 cycles of latency per tile
+          float mxs[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
+          for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(s[k], s[8 + k]);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
-#if WF_POLY_EVERY > 0
-            // masked (-inf) logits exist only on DIAG tiles: those stay on MUFU (exact 0)
-            const bool poly = !DIAG && ((c * 16 + i) % WF_POLY_EVERY) == WF_POLY_EVERY - 1;
-            const float2 p = poly ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
-#else
-            const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-#endif
-            rs2[c] = fadd2(rs2[c], p);
-            pk[i] = pack_bf16x2(p.x, p.y);
+          for (int c = 16; c < 128; c += 16)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(mxs[k], fmaxf(s[c + k], s[c + 8 + k]));
+          const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                                 fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+          const float mcand = mx * a.scale_log2;
+          const bool need = mcand > m + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float mnew = fmaxf(m, mcand);
+            const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mnew);
+            if (j > 0 || has_state) {
+              // PV_t(j-1) retired with the S_t(j) commit (issued before it)
+#pragma unroll
+              for (int c = 0; c < DP / 16; ++c) {
+                uint32_t r[16];
+                tmem_ld16(tl + cO + c * 16, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                tmem_st16(tl + cO + c * 16, r);
+              }
+            }
+            l *= alpha;
+            m = mnew;
           }
-          tmem_st16(tl + cS + c * 16, pk);
+          tl_stamp(a.tl, tlon && lane == 0 && wq == 0, 1 + t, j, 3);
+          rs = exps((m == -INFINITY) ? 0.f : m);
         }
-        const float2 rsa = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
-        const float rs = rsa.x + rsa.y;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar[B_P + 4 * t]);
