@@ -163,3 +163,23 @@ def test_block_fwd_chained_blocks(causal, case):
         o, l = to_f64(ob), lse.cpu().double().numpy()
     eo, el = np.abs(o - o_ref).max(), _cmp_lse(l, l_ref)
     assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_block_fwd_growing_logits(causal):
+    """Logits that grow by orders of magnitude along the key sequence: the forward's fast
+    path (exponentials against the running max, no max pass) must fall back to the row max
+    whenever a tile's logits exceed the running max by 2^6 (log2 domain); values and LSE
+    still match the oracle.  (The ramp also makes later tiles dominate each row.)"""
+    wf = _wf()
+    N, h, d = 1024, 2, 128
+    q, k, v, _ = make_qkv_do(N, h, d, seed=17)
+    ramp = torch.linspace(0.05, 150.0, N).view(N, 1, 1)  # tile-to-tile max jumps of 2^6 and more
+    k = (k.float() * ramp).to(torch.bfloat16)
+    qd, kd, vd = (t.cuda() for t in (q, k, v))
+    _, ob, lse = wf.block_fwd(qd, kd, vd, causal=causal, chunk=N if causal else 0, qstart=[0] if causal else None,
+                              kstart=[0] if causal else None)
+    torch.cuda.synchronize()
+    o_ref, l_ref = attention_fwd(to_f64(q), to_f64(k), to_f64(v), causal=causal)
+    eo, el = np.abs(to_f64(ob) - o_ref).max(), _cmp_lse(lse.cpu().double().numpy(), l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
