@@ -22,7 +22,6 @@ using namespace sm100;
 
 namespace {
 
-constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
 struct BwdCfg {
@@ -281,17 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ss = ii & 1;
       const float* slse = stat + ss * 256 + hf * 64;
       const float* sdd = stat + ss * 256 + 128 + hf * 64;
-      mbar_wait(&bar[B_SF + ss], (ii >> 1) & 1);  // stats landed
-      {
-        // convert the tile's statistics once, negated for packed FMAs:
-        // lse -> -lse * log2(e) (-inf for query rows with no key at all, so exp2 gives 0
-        // without a branch), D -> -D / sqrt(d)
-        float* sst = stat + ss * 256;
-        const int tc = threadIdx.x - 128;
-        const float x = sst[tc];
-        sst[tc] = tc < 128 ? (x == -INFINITY ? -INFINITY : -x * kLog2e) : -x * a.scale;
-        named_bar_sync(2, kCompute);
-      }
+      // stats landed: -lse log2(e) (-inf for query rows with no key at all, so exp2 gives
+      // 0 without a branch) and -D / sqrt(d), converted once per call for the packed FMAs
+      mbar_wait(&bar[B_SF + ss], (ii >> 1) & 1);
       mbar_wait(&bar[B_S], ii & 1);
       tc_fence_after();
       tl_stamp(a.tl, tlon && threadIdx.x == 128, 1, ii, 0);
@@ -300,11 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(tl + hf * 64, sv[0]);
       tmem_ld32(tl + hf * 64 + 32, sv[1]);
       tmem_wait_ld();
-      // all of S^T is in registers: P may now overwrite columns [0, 64) (after both halves
-      // have loaded: the named barrier), and the dQ drain may park data in [64, 128)
+      // all of S^T is in registers: P may now overwrite columns [0, 64) (after both warps
+      // of this lane quadrant have loaded: the named barrier of the pair), and the dQ drain
+      // may park data in [64, 128)
       tc_fence_before();
       mbar_arrive(&bar[B_SL]);
-      named_bar_sync(3, kCompute);
+      named_bar_sync(4 + wq, 64);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const uint32_t* rr = sv[c];

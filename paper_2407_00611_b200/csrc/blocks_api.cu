@@ -189,8 +189,19 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
   }
   a.scale = 1.f / std::sqrt(static_cast<float>(head_dim));
   a.scale_log2 = 1.4426950408889634f * a.scale;
-  a.lse = lse;
-  a.dsum = dsum;
+  // the kernel takes -LSE log2(e) and -D / sqrt(d) (the runtime stores them that way once
+  // per call); convert the caller's natural-log LSE and D into stream-ordered scratch
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ns = static_cast<int64_t>(heads) * nq;
+  float* conv = nullptr;
+  if (ns > 0) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&conv), 2 * ns * sizeof(float), st) != cudaSuccess)
+      return set_err(WF_ERR_CUDA, "wf_block_bwd: scratch allocation failed");
+    cudaError_t ce = launch_stats_convert(lse, dsum, conv, conv + ns, ns, a.scale, st);
+    if (ce != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(ce));
+  }
+  a.lse = conv;
+  a.dsum = conv ? conv + ns : nullptr;
   a.dq_acc = dq_acc;
   a.dk_acc = dk_acc;
   a.dv_acc = dv_acc;
@@ -198,9 +209,12 @@ extern "C" wf_status wf_block_bwd(const void* q, const void* k, const void* v, c
   a.stat_blk = nq > 0 ? nq : WF_TILE;
   CUtensorMap tq, tk, tv, tdo;
   if (!make_tmap_rows(&tq, q, nq > 0 ? nq : WF_TILE, heads, head_dim) || !make_tmap_rows(&tk, k, nk, heads, head_dim) ||
-      !make_tmap_rows(&tv, v, nk, heads, head_dim) || !make_tmap_rows(&tdo, dO, nq > 0 ? nq : WF_TILE, heads, head_dim))
+      !make_tmap_rows(&tv, v, nk, heads, head_dim) || !make_tmap_rows(&tdo, dO, nq > 0 ? nq : WF_TILE, heads, head_dim)) {
+    if (conv) cudaFreeAsync(conv, st);
     return set_err(WF_ERR_ARG, "wf_block_bwd: TMA map encode failed (alignment?)");
-  cudaError_t e = launch_block_bwd(tq, tk, tv, tdo, a, head_dim, static_cast<cudaStream_t>(stream));
+  }
+  cudaError_t e = launch_block_bwd(tq, tk, tv, tdo, a, head_dim, st);
+  if (conv) cudaFreeAsync(conv, st);
   if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
   return WF_OK;
 }

@@ -118,8 +118,9 @@ struct BwdArgs {
   PosTable qpos, kpos;
   float scale_log2;               // log2(e) / sqrt(head_dim)
   float scale;                    // 1 / sqrt(head_dim)
-  const float* lse;               // [heads, nq] natural-log LSE of the query rows (final forward)
-  const float* dsum;              // [heads, nq] D = rowsum(dO o O)
+  const float* lse;               // [heads, nq] -LSE log2(e) of the query rows (final forward LSE,
+                                  // natural log, converted by launch_dsum / launch_stats_convert)
+  const float* dsum;              // [heads, nq] -D / sqrt(d), D = rowsum(dO o O)
   float* dq_acc;                  // fp32 [nq, heads, D] accumulated with atomics
   float* dk_acc;                  // fp32 [nk, heads, D] (accumulate if dkv_accumulate)
   float* dv_acc;
@@ -193,8 +194,11 @@ struct SumArgs {
   __nv_bfloat16* out;
 };
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
-cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* dsum, int rows, int heads, int D,
-                        cudaStream_t s);
+cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, const float* lse, float* nd, float* nl,
+                        int rows, int heads, int D, float scale, cudaStream_t s);
+// nl = -lse log2(e) (-inf kept), nd = -dsum scale, n elements
+cudaError_t launch_stats_convert(const float* lse, const float* dsum, float* nl, float* nd, int64_t n, float scale,
+                                 cudaStream_t s);
 cudaError_t launch_sum(const SumArgs& a, cudaStream_t s);
 }  // namespace wf
 

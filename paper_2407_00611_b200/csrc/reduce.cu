@@ -2,7 +2,9 @@
 //   * wf_merge_kernel  : Alg. 1 l.11 ReduceScatter_combine:
 //                        L = logsumexp_a lse_a, O = sum_a exp(lse_a - L) O_a over the C
 //                        partials of this rank's rows -> bf16 O, fp32 LSE.
-//   * wf_dsum_kernel   : D = rowsum(dO o O) (flash-attention backward preprocess; reading c12).
+//   * wf_dsum_kernel   : D = rowsum(dO o O) (flash-attention backward preprocess; reading c12),
+//                        stored with the LSE as the block backward consumes them:
+//                        -D / sqrt(d) and -LSE log2(e).
 //   * wf_sum_kernel    : the backward team reductions (reading c11): out = sum_j part_j
 //                        (fp32 partials -> bf16).
 // All are bandwidth kernels: 16-byte vector loads/stores, grid-stride, grid sized from
@@ -74,7 +76,8 @@ __global__ void wf_merge_kernel(MergeArgs a) {
 
 // D[h][row] = sum_d dO[row,h,d] * O[row,h,d]; one 8-lane group per (row, head).
 __global__ void wf_dsum_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
-                               float* __restrict__ dsum, int rows, int heads, int D) {
+                               const float* __restrict__ lse, float* __restrict__ nd, float* __restrict__ nl,
+                               int rows, int heads, int D, float scale) {
   const int lanes = 8;
   const int64_t total = static_cast<int64_t>(rows) * heads;
   const int sub = threadIdx.x % lanes;
@@ -94,7 +97,25 @@ __global__ void wf_dsum_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_
     }
 #pragma unroll
     for (int o = lanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
-    if (sub == 0) dsum[static_cast<int64_t>(head) * rows + row] = acc;
+    if (sub == 0) {
+      // the block backward's statistics, converted once per call for its packed FMAs:
+      // -D / sqrt(d) and -LSE log2(e) (-inf kept for query rows without any key)
+      const int64_t i = static_cast<int64_t>(head) * rows + row;
+      nd[i] = -acc * scale;
+      const float x = lse[i];
+      nl[i] = x == -INFINITY ? -INFINITY : -x * 1.4426950408889634f;
+    }
+  }
+}
+
+// the same conversion for statistics computed elsewhere (wf_block_bwd's D and LSE)
+__global__ void wf_stats_convert_kernel(const float* __restrict__ lse, const float* __restrict__ dsum,
+                                        float* __restrict__ nl, float* __restrict__ nd, int64_t n, float scale) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float x = lse[i];
+    nl[i] = x == -INFINITY ? -INFINITY : -x * 1.4426950408889634f;
+    nd[i] = -dsum[i] * scale;
   }
 }
 
@@ -144,11 +165,18 @@ cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* dsum, int rows, int heads, int D,
-                        cudaStream_t s) {
+cudaError_t launch_dsum(const __nv_bfloat16* dO, const __nv_bfloat16* O, const float* lse, float* nd, float* nl,
+                        int rows, int heads, int D, float scale, cudaStream_t s) {
   if (D % 8) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(rows) * heads * 8;
-  wf_dsum_kernel<<<grid_for(work, 256), 256, 0, s>>>(dO, O, dsum, rows, heads, D);
+  wf_dsum_kernel<<<grid_for(work, 256), 256, 0, s>>>(dO, O, lse, nd, nl, rows, heads, D, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_convert(const float* lse, const float* dsum, float* nl, float* nd, int64_t n, float scale,
+                                 cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  wf_stats_convert_kernel<<<grid_for(n, 256), 256, 0, s>>>(lse, dsum, nl, nd, n, scale);
   return cudaGetLastError();
 }
 

@@ -50,7 +50,8 @@ struct RankBufs {
   float* rs_o = nullptr;                             // [C][n rows] fp32 partials of my rows
   float* rs_lse = nullptr;                           // [C][h][n]
   // backward
-  float* dsum = nullptr;                             // [h][n]
+  float* dsum = nullptr;                             // [h][n] -D / sqrt(d) of my rows
+  float* nlse = nullptr;                             // [h][n] -LSE log2(e) of my rows
   bf16* t_do = nullptr;                              // team dO (C*n rows)
   float *t_lse = nullptr, *t_dsum = nullptr;         // [C][h][n]
   bf16 *pq[2] = {nullptr, nullptr}, *pdo[2] = {nullptr, nullptr};
@@ -322,6 +323,7 @@ void carve_rank(const Geo& g, RankBufs& b, CarveList& items, bool copies) {
     add(&b.lse_state, C * h * n * 4);
   }
   add(&b.dsum, h * n * 4);
+  add(&b.nlse, h * n * 4);
   for (int s = 0; s < (g.R > 1 ? 2 : 1); ++s) {
     add(&b.pdq[s], team * 4);
     if (g.R > 1) {
@@ -1076,14 +1078,19 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
   const bool nt = (ctx->debug & WF_DEBUG_NO_TRANSFER) != 0;
   WCK(ipc_barrier(ctx, st));
 
-  // D = rowsum(dO o O) on own rows (reading c12).
+  // D = rowsum(dO o O) on own rows (reading c12), stored with this rank's LSE in the form
+  // the block backward consumes (-D / sqrt(d), -LSE log2(e)); these are what the team
+  // gathers and the Q-package carry (same bytes as the raw statistics).
   for (int r = 0; r < P; ++r) {
     if (!local(ctx, r) || ctx->dry) continue;
-    WCK(kcheck(ctx, launch_dsum(L(r, dO, n * E), L(r, O, n * E), B(ctx, r).dsum, g.n, g.h, g.d, st), "dsum"));
+    WCK(kcheck(ctx,
+               launch_dsum(L(r, dO, n * E), L(r, O, n * E), L(r, LSE, n * h), B(ctx, r).dsum, B(ctx, r).nlse, g.n,
+                           g.h, g.d, 1.f / std::sqrt(static_cast<float>(g.d)), st),
+               "dsum"));
   }
   auto qteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).qt) : L(r, Q, n * E); };
   auto doteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).t_do) : L(r, dO, n * E); };
-  auto lseteam = [&](int r) -> const float* { return C > 1 ? lp(r, B(ctx, r).t_lse) : L(r, LSE, n * h); };
+  auto lseteam = [&](int r) -> const float* { return C > 1 ? lp(r, B(ctx, r).t_lse) : lp(r, B(ctx, r).nlse); };
   auto dsteam = [&](int r) -> const float* { return C > 1 ? lp(r, B(ctx, r).t_dsum) : lp(r, B(ctx, r).dsum); };
   auto kteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).kt) : L(r, K, n * E); };
   auto vteam = [&](int r) -> const bf16* { return C > 1 ? lp(r, B(ctx, r).vt) : L(r, V, n * E); };
@@ -1119,7 +1126,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
         xs.push_back(x);
         Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
-        y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
+        y.segs.push_back({lp(r, B(ctx, r).nlse), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
         y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
         xs.push_back(y);
       }
@@ -1169,7 +1176,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
         ba.kpos = units_table(g, u, 1);
         ba.scale = 1.f / std::sqrt(static_cast<float>(g.d));
         ba.scale_log2 = 1.4426950408889634f * ba.scale;
-        ba.lse = own ? L(me, LSE, n * h) : b.t_lse + jm * h * n;
+        ba.lse = own ? b.nlse : b.t_lse + jm * h * n;
         ba.dsum = own ? b.dsum : b.t_dsum + jm * h * n;
         ba.stat_blk = g.n;
         ba.dq_acc = b.pdq[0] + jm * n * E;
@@ -1204,7 +1211,7 @@ wf_status backward(wf_ctx* ctx, const Geo& g, const bf16* dO, const bf16* Q, con
           x.segs.push_back({L(r, dO, n * E), at(lp(p, B(ctx, p).t_do), j * n * E), n * E * 2});
           xs.push_back(x);
           Xfer y{1, WF_KIND_AG_STATS, -1, r, p, r, {}};
-          y.segs.push_back({L(r, LSE, n * h), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
+          y.segs.push_back({lp(r, B(ctx, r).nlse), at(lp(p, B(ctx, p).t_lse), j * h * n), h * n * 4});
           y.segs.push_back({lp(r, B(ctx, r).dsum), at(lp(p, B(ctx, p).t_dsum), j * h * n), h * n * 4});
           xs.push_back(y);
           if (g.paper && !g.direct) {

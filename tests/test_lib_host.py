@@ -104,7 +104,7 @@ def test_bad_config_is_config_error(wf):
 
 
 def test_workspace_sized_by_regime():
-    # one GPU keeps only the dQ accumulator and D (bf16 O and dK/dV leave the
+    # one GPU keeps only the dQ accumulator and the statistics (bf16 O and dK/dV leave the
     # kernels directly); the C = 1 ring at P = 8 keeps two K/V slots, the fp32 state, two
     # dQ / Q-package slots, the home dQ and the dK/dV accumulators -- and no receive slots
     # for pulled partials (peer memory reads them in place).
@@ -112,9 +112,10 @@ def test_workspace_sized_by_regime():
     al = lambda b: (b + 1023) // 1024 * 1024  # noqa: E731
     E, h = 32 * 128, 32
     n = 32768
-    assert wf.workspace_bytes(1, 1, 32768, 32, 128, True) == 4096 + al(n * E * 4) + al(h * n * 4)
+    # dQ accumulator, -D / sqrt(d), -LSE log2(e)
+    assert wf.workspace_bytes(1, 1, 32768, 32, 128, True) == 4096 + al(n * E * 4) + 2 * al(h * n * 4)
     n = 131072 // 8
-    ring = (4096 + 4 * al(n * E * 2) + al(n * E * 4) + al(h * n * 4) + al(h * n * 4)
+    ring = (4096 + 4 * al(n * E * 2) + al(n * E * 4) + al(h * n * 4) + 2 * al(h * n * 4)
             + 2 * (al(n * E * 4) + 2 * al(n * E * 2) + 2 * al(h * n * 4)) + al(n * E * 4) + 2 * al(n * E * 4))
     assert wf.workspace_bytes(8, 1, 131072, 32, 128, True) == ring
     # the paper regime (C^2 | P) needs no merge / dQ-sum receive slots; the extension does
