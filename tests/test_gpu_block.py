@@ -183,3 +183,55 @@ def test_block_fwd_growing_logits(causal):
     o_ref, l_ref = attention_fwd(to_f64(q), to_f64(k), to_f64(v), causal=causal)
     eo, el = np.abs(to_f64(ob) - o_ref).max(), _cmp_lse(lse.cpu().double().numpy(), l_ref)
     assert eo <= O_TOL and el <= LSE_TOL, (eo, el)
+
+
+def _random_case(seed):
+    """A seeded random block layout: head_dim, heads, tile counts, mask and (causal) chunk
+    starts drawn at random -- disjoint key chunks, query chunks possibly before every key."""
+    rng = np.random.default_rng(seed)
+    d = int(rng.choice([64, 72, 128]))
+    h = int(rng.integers(1, 4))
+    causal = bool(rng.integers(0, 2))
+    chunk = 128 * int(rng.choice([1, 2]))
+    nqc, nkc = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    slots = rng.permutation(16)[: nqc + nkc] * chunk  # global chunk positions
+    qstart = [int(x) for x in slots[:nqc]]
+    kstart = [int(x) for x in slots[nqc:]]
+    if not causal:
+        chunk, qstart, kstart = 0, None, None
+    return d, h, causal, chunk, nqc, nkc, qstart, kstart
+
+
+@pytest.mark.parametrize("seed", list(range(10)))
+def test_block_fwd_bwd_random_layouts(seed):
+    """Randomised layouts of both block kernels against the oracle (forward: O, LSE;
+    backward: dQ, dK, dV from the oracle's block backward with the exact statistics)."""
+    wf = _wf()
+    d, h, causal, chunk, nqc, nkc, qstart, kstart = _random_case(seed)
+    c = chunk if causal else 128 * 2
+    nq, nk = nqc * c, nkc * c
+    q, k, v, do = make_qkv_do(max(nq, nk), h, d, seed=100 + seed, peaky=bool(seed % 2))
+    q, do = q[:nq], do[:nq]
+    k, v = k[:nk], v[:nk]
+    qp = _pos(chunk, qstart) if causal else np.arange(nq)
+    kp = _pos(chunk, kstart) if causal else np.arange(nk)
+    dev = torch.device("cuda")
+    _, ob, lse = wf.block_fwd(q.cuda(), k.cuda(), v.cuda(), causal=causal, chunk=chunk, qstart=qstart,
+                              kstart=kstart)
+    torch.cuda.synchronize()
+    o_ref, l_ref = attention_fwd(to_f64(q), to_f64(k), to_f64(v), qp, kp, causal)
+    eo, el = np.abs(to_f64(ob) - o_ref).max(), _cmp_lse(lse.cpu().double().numpy(), l_ref)
+    assert eo <= O_TOL and el <= LSE_TOL, (seed, eo, el)
+    dd = np.ascontiguousarray(np.sum(to_f64(do) * o_ref, axis=2).T)
+    dq_r, dk_r, dv_r = o_block_bwd(to_f64(q), to_f64(k), to_f64(v), to_f64(do), l_ref, dd, qp, kp, causal)
+    dq = torch.zeros((nq, h, d), dtype=torch.float32, device=dev)
+    dk = torch.zeros((nk, h, d), dtype=torch.float32, device=dev)
+    dv = torch.zeros((nk, h, d), dtype=torch.float32, device=dev)
+    wf.block_bwd(q.cuda(), k.cuda(), v.cuda(), do.cuda(), torch.tensor(l_ref, dtype=torch.float32, device=dev),
+                 torch.tensor(dd, dtype=torch.float32, device=dev), dq, dk, dv, causal=causal, chunk=chunk,
+                 qstart=qstart, kstart=kstart)
+    torch.cuda.synchronize()
+    for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
+        scale = max(np.abs(ref).max(), 1e-30)
+        err = np.abs(got.cpu().double().numpy() - ref).max() / scale
+        assert err <= G_TOL, (seed, name, err)
