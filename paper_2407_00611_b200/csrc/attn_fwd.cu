@@ -25,9 +25,6 @@ using namespace sm100;
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
-#ifndef WF_FWD_PAIR
-#define WF_FWD_PAIR 0  // 1: head_dim 128 runs the CTA-pair kernel (experiment, slower: profiles/r02_fwd_experiments.md)
-#endif
 #ifndef WF_FWD_FASTMAX
 #define WF_FWD_FASTMAX 1  // 1: skip the row-max pass while the running max stays valid (see tile())
 #endif
@@ -436,360 +433,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
-// ---------------------------------------------------------------- CTA-pair forward (head_dim 128)
-// A cluster of two CTAs on two SMs owns two query tiles, one per CTA.  Both S = Q K^T and
-// O += P V are M = 256 tcgen05 MMAs issued by the even CTA (cta_group::2): each CTA holds
-// its own Q rows, P rows and O rows, and HALF of every K tile (64 keys) and of every V tile
-// (64 head-dim columns), so an SM reads 32 KB of K/V per key tile instead of 64 KB, and one
-// MMA instruction does the work of two.  With a single query tile per SM the tensor
-// memory holds three S buffers besides O (S_b [128 b, 128 b + 128), O [384, 512)): the
-// tensor pipe runs S(j+2) before P V(j), so S(j+1) never queues behind the P V that waits
-// for the softmax of tile j-1, the softmax runs back to back and the per-tile chain
-// S -> softmax -> P V of the two-tile kernel leaves the critical path.
-// The O rescale of the slow path (row max moved) waits for P V(j-1) on its own barrier.
-struct FwdPairCfg {
-  static constexpr int PANEL = 128 * 128;        // [128 rows x 64 bf16]
-  static constexpr int HPANEL = 64 * 128;        // [64 rows x 64 bf16]
-  static constexpr int QB = 2 * PANEL;           // this CTA's query tile
-  static constexpr int KB = 2 * HPANEL;          // this CTA's 64 keys x 128 dims of a K tile
-  static constexpr int VB = PANEL;               // 128 keys x this CTA's 64 dims of a V tile
-  static constexpr int KS = 4, VS = 4;           // ring stages
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = QB;
-  static constexpr int OFF_V = OFF_K + KS * KB;
-  static constexpr int OFF_BAR = OFF_V + VS * VB;
-  static constexpr int SMEM = OFF_BAR + 256;
-  static_assert(SMEM <= 232448, "shared memory budget");
-};
-// barriers (same offsets in both CTAs; Q/K/V-full and P-full are used in the even CTA only)
-enum { PB_Q = 0, PB_K = 1, PB_KE = 5, PB_V = 9, PB_VE = 13, PB_S = 17, PB_P = 20, PB_PV = 23, PB_OF = 25, PB_NUM = 26 };
-constexpr int kSBuf = 3;  // S buffers in tensor memory (O after them)
-constexpr int kPairThreads = 8 * 32;  // TMA, MMA, 2 idle, 4 softmax warps
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
-    wf_block_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FwdArgs a) {
-  using Cfg = FwdPairCfg;
-  constexpr int D = 128;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BAR + PB_NUM * 8);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t cr = cluster_ctarank();
-  const int nqt = a.nq / WF_TILE;
-  const int npairs = (nqt + 1) >> 1;
-  const int pidx = blockIdx.x >> 1;
-  const int pair = a.causal ? (npairs - 1 - pidx) : pidx;  // heavy pairs first
-  const int head = blockIdx.y;
-  const int t0 = pair * 2;                                  // the pair's first query tile
-  const bool hasB = (t0 + 1) < nqt;
-  const bool mine = cr == 0 || hasB;                        // this CTA owns a query tile
-  const int qtile = t0 + (mine ? static_cast<int>(cr) : 0);
-  const int qposA = a.causal ? tile_gpos(a.qpos, t0) : t0 * WF_TILE;
-  const int qposB = (a.causal && hasB) ? tile_gpos(a.qpos, t0 + 1) : (t0 + 1) * WF_TILE;
-  const int qpos = cr == 0 ? qposA : qposB;
-  const bool has_state = a.o_in != nullptr;
-  const bool tlon = a.tl && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.tl_cta;
-  const int qbound = hasB ? max(qposA, qposB) : qposA;
-  auto kv_iter = [&]() { return VisIter<true>(a.kpos, a.causal != 0, qbound); };
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023) __trap();
-    mbar_init(&bar[PB_Q], 1);
-    for (int i = 0; i < Cfg::KS; ++i) {
-      mbar_init(&bar[PB_K + i], 1);
-      mbar_init(&bar[PB_KE + i], 1);
-    }
-    for (int i = 0; i < Cfg::VS; ++i) {
-      mbar_init(&bar[PB_V + i], 1);
-      mbar_init(&bar[PB_VE + i], 1);
-    }
-    for (int i = 0; i < kSBuf; ++i) {
-      mbar_init(&bar[PB_S + i], 1);
-      mbar_init(&bar[PB_P + i], 8);  // one arrive per softmax warp of both CTAs
-    }
-    for (int i = 0; i < 2; ++i) mbar_init(&bar[PB_PV + i], 1);
-    mbar_init(&bar[PB_OF], 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    tmem_alloc2(tmem_slot, 512);
-    tmem_relinquish2();
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producers (both CTAs)
-    // every load completes on the even CTA's barrier, which expects the bytes of both CTAs
-    if (lane == 0) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      if (cr == 0) mbar_arrive_expect_tx(&bar[PB_Q], 2 * Cfg::QB);
-      for (int p = 0; p < 2; ++p)
-        tma_load_3d_pair(smem + Cfg::OFF_Q + p * Cfg::PANEL, &tmQ, &bar[PB_Q], p * 64, head, qtile * WF_TILE);
-      int jj = 0, jt, kp;
-      for (auto it = kv_iter(); it.next(a.kpos, jt, kp); ++jj) {
-        const int st = jj % Cfg::KS;
-        if (jj >= Cfg::KS) mbar_wait(&bar[PB_KE + st], ((jj - Cfg::KS) / Cfg::KS) & 1);
-        if (cr == 0) mbar_arrive_expect_tx(&bar[PB_K + st], 2 * Cfg::KB);
-        uint8_t* sk = smem + Cfg::OFF_K + st * Cfg::KB;
-        for (int p = 0; p < 2; ++p)
-          tma_load_3d_pair(sk + p * Cfg::HPANEL, &tmK, &bar[PB_K + st], p * 64, head, jt * WF_TILE + cr * 64);
-      }
-    } else if (lane == 1) {
-      tma_prefetch_desc(&tmV);
-      int jj = 0, jt, kp;
-      for (auto it = kv_iter(); it.next(a.kpos, jt, kp); ++jj) {
-        const int st = jj % Cfg::VS;
-        if (jj >= Cfg::VS) mbar_wait(&bar[PB_VE + st], ((jj - Cfg::VS) / Cfg::VS) & 1);
-        if (cr == 0) mbar_arrive_expect_tx(&bar[PB_V + st], 2 * Cfg::VB);
-        tma_load_3d_pair(smem + Cfg::OFF_V + st * Cfg::VB, &tmV, &bar[PB_V + st], cr * 64, head, jt * WF_TILE);
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (even CTA)
-    // order: S(0), S(1); then per key tile j: S(j+2), P V(j).  S(j+2) overwrites the buffer
-    // of P(j-1), whose P V was issued earlier in the same in-order tensor pipe.
-    if (cr == 0 && lane == 0) {
-      constexpr uint32_t idS = idesc_bf16_f32(256, 128, 0, 0);  // Q (K-major) x K (K-major)
-      constexpr uint32_t idO = idesc_bf16_f32(256, D, 0, 1);    // P (TMEM) x V (MN-major)
-      auto issue_s = [&](int j) {
-        const int st = j % Cfg::KS;
-        mbar_wait(&bar[PB_K + st], (j / Cfg::KS) & 1);
-        tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q);
-        const uint32_t sK = smem_u32(smem + Cfg::OFF_K + st * Cfg::KB);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const int p = k >> 2, kk = k & 3;
-          mma2_ss(tbase + (j % kSBuf) * 128, smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024),
-                  smem_desc_sw128(sK + p * Cfg::HPANEL + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
-        }
-        mma2_commit_mc(&bar[PB_S + j % kSBuf], 0x3);
-        mma2_commit_mc(&bar[PB_KE + st], 0x3);
-      };
-      auto issue_pv = [&](int j) {
-        const int st = j % Cfg::VS;
-        mbar_wait(&bar[PB_P + j % kSBuf], (j / kSBuf) & 1);
-        tl_stamp(a.tl, tlon, 0, j, 2);
-        mbar_wait(&bar[PB_V + st], (j / Cfg::VS) & 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(smem + Cfg::OFF_V + st * Cfg::VB);
-#pragma unroll
-        for (int k = 0; k < WF_TILE / 16; ++k)
-          mma2_ts(tbase + kSBuf * 128, tbase + (j % kSBuf) * 128 + k * 8, smem_desc_sw128(sV + k * 2048, Cfg::PANEL, 1024), idO,
-                  (j > 0 || has_state || k > 0) ? 1u : 0u);
-        mma2_commit_mc(&bar[PB_PV + (j & 1)], 0x3);
-        mma2_commit_mc(&bar[PB_VE + st], 0x3);
-      };
-      const int nvis = kv_iter().count(a.kpos);
-      mbar_wait(&bar[PB_Q], 0);
-      for (int j = 0; j < kSBuf - 1 && j < nvis; ++j) issue_s(j);
-      for (int j = 0; j < nvis; ++j) {
-        tl_stamp(a.tl, tlon, 0, j, 0);
-        if (j + kSBuf - 1 < nvis) issue_s(j + kSBuf - 1);
-        tl_stamp(a.tl, tlon, 0, j, 1);
-        issue_pv(j);
-        tl_stamp(a.tl, tlon, 0, j, 3);
-      }
-      mma2_commit_mc(&bar[PB_OF], 0x3);
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax + epilogue
-    const int wq = warp & 3;
-    const int row = wq * 32 + lane;
-    const uint32_t tl = tbase + (static_cast<uint32_t>(wq * 32) << 16);
-    constexpr uint32_t cO = kSBuf * 128;
-    const int grow = qtile * WF_TILE + row;
-    const size_t orow = (static_cast<size_t>(grow) * a.heads + head) * D;
-    const bool tls = tlon && lane == 0 && wq == 0;
-    float m = -INFINITY, l = 0.f;
-    if (has_state && mine) {
-      const float ls = a.lse_in[stat_index(head, grow, a.heads, a.lse_blk)];
-      m = ls * kLog2e;
-      l = (ls == -INFINITY) ? 0.f : 1.f;
-#pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
-        uint32_t r[16];
-        const float4* src = reinterpret_cast<const float4*>(a.o_in + orow + c * 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 v = src[i];
-          r[4 * i] = __float_as_uint(v.x);
-          r[4 * i + 1] = __float_as_uint(v.y);
-          r[4 * i + 2] = __float_as_uint(v.z);
-          r[4 * i + 3] = __float_as_uint(v.w);
-        }
-        tmem_st16(tl + cO + c * 16, r);
-      }
-      tmem_wait_st();
-    }
-    int j = 0;
-    auto tile = [&](auto diag_c, const int kind) {
-      constexpr bool DIAG = decltype(diag_c)::value;
-      const uint32_t cS = (j % kSBuf) * 128;
-      mbar_wait(&bar[PB_S + j % kSBuf], (j / kSBuf) & 1);
-      tc_fence_after();
-      tl_stamp(a.tl, tls, 1, j, 0);
-      float s[128];
-      {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        tmem_ld32(tl + cS + 0, r0);
-        tmem_ld32(tl + cS + 32, r1);
-        tmem_ld32(tl + cS + 64, r2);
-        tmem_ld32(tl + cS + 96, r3);
-        tmem_wait_ld();
-        tl_stamp(a.tl, tls, 1, j, 2);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = __uint_as_float(r0[i]);
-          s[32 + i] = __uint_as_float(r1[i]);
-          s[64 + i] = __uint_as_float(r2[i]);
-          s[96 + i] = __uint_as_float(r3[i]);
-        }
-      }
-      if constexpr (DIAG) {
-        const int lim = kind == 0 ? -1 : row;
-#pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = c > lim ? -INFINITY : s[c];
-      }
-      auto exps = [&](const float mm) -> float {
-        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mm, -mm);
-        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
-            const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-            rs2[c] = fadd2(rs2[c], p);
-            pk[i] = pack_bf16x2(p.x, p.y);
-          }
-          tmem_st16(tl + cS + c * 16, pk);
-        }
-        const float2 rsa = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
-        return rsa.x + rsa.y;
-      };
-      // fast path / slow path as in the two-tile kernel (see tile() there)
-      float rs = 0.f;
-      bool slow = !WF_FWD_FASTMAX || __any_sync(0xffffffffu, m == -INFINITY);
-      if (!slow) {
-        rs = exps(m);
-        slow = __any_sync(0xffffffffu, !(rs < 1.8446744e19f));
-      }
-      if (slow) {
-        float mxs[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(s[k], s[8 + k]);
-#pragma unroll
-        for (int c = 16; c < 128; c += 16)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mxs[k] = fmaxf(mxs[k], fmaxf(s[c + k], s[c + 8 + k]));
-        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
-        const float mcand = mx * a.scale_log2;
-        const bool need = mcand > m + 8.0f;
-        if (__any_sync(0xffffffffu, need)) {
-          const float mnew = fmaxf(m, mcand);
-          const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mnew);
-          if (j > 0 || has_state) {
-            if (j > 0) {
-              // O must hold P V(j-1) before it is rescaled
-              mbar_wait(&bar[PB_PV + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-              tc_fence_after();
-            }
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-              uint32_t r[16];
-              tmem_ld16(tl + cO + c * 16, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tmem_st16(tl + cO + c * 16, r);
-            }
-          }
-          l *= alpha;
-          m = mnew;
-        }
-        tl_stamp(a.tl, tls, 1, j, 3);
-        rs = exps((m == -INFINITY) ? 0.f : m);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&bar[PB_P + j % kSBuf], 0);
-      tl_stamp(a.tl, tls, 1, j, 1);
-      l += rs;
-      ++j;
-    };
-    int jt, kp;
-    for (auto it = kv_iter(); it.next(a.kpos, jt, kp);) {
-      const int kind = !mine ? 0 : (!a.causal ? 1 : (kp > qpos ? 0 : (kp == qpos ? 2 : 1)));
-      if (kind == 1)
-        tile(std::integral_constant<bool, false>{}, kind);
-      else
-        tile(std::integral_constant<bool, true>{}, kind);
-    }
-    // epilogue
-    mbar_wait(&bar[PB_OF], 0);
-    tc_fence_after();
-    if (mine) {
-      const bool have_o = j > 0 || has_state;
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      a.lse_out[stat_index(head, grow, a.heads, a.lse_blk)] = l > 0.f ? (m + __log2f(l)) * kLn2 : -INFINITY;
-#pragma unroll
-      for (int c = 0; c < D / 16; ++c) {
-        uint32_t r[16];
-        if (have_o) {
-          tmem_ld16(tl + cO + c * 16, r);
-          tmem_wait_ld();
-        }
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = have_o ? __uint_as_float(r[i]) * inv : 0.f;
-        if (a.o_out_f32) {
-          float4* dst = reinterpret_cast<float4*>(a.o_out_f32 + orow + c * 16);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-        if (a.o_out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(a.o_out_bf16 + orow + c * 16);
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  if (warp == 1) tmem_dealloc2(tbase, 512);
-}
-
-cudaError_t launch_fwd_pair(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
-                            cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(wf_block_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         FwdPairCfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  dim3 grid(2 * ((a.nq / WF_TILE + 1) / 2), a.heads);
-  FwdArgs b = a;
-  b.tl = timeline_buffer();
-  b.tl_cta = timeline_cta();
-  wf_block_fwd_pair_kernel<<<grid, kPairThreads, FwdPairCfg::SMEM, s>>>(tq, tk, tv, b);
-  return cudaGetLastError();
-}
-
 template <int D>
 cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                          cudaStream_t s) {
@@ -810,13 +453,11 @@ cudaError_t launch_fwd_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
 
 }  // namespace
 
-int fwd_k_box_rows(int D) { return (WF_FWD_PAIR && D == 128) ? 64 : WF_TILE; }
-
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s) {
   if (a.nq <= 0 || a.nq % WF_TILE || a.nk % WF_TILE) return cudaErrorInvalidValue;
   switch (D) {
-    case 128: return WF_FWD_PAIR ? launch_fwd_pair(tq, tk, tv, a, s) : launch_fwd_d<128>(tq, tk, tv, a, s);
+    case 128: return launch_fwd_d<128>(tq, tk, tv, a, s);
     case 64: return launch_fwd_d<64>(tq, tk, tv, a, s);
     case 72: return launch_fwd_d<72>(tq, tk, tv, a, s);
     default: return cudaErrorInvalidValue;

@@ -159,8 +159,7 @@ extern "C" wf_status wf_block_fwd(const void* q, const void* k, const void* v, i
   a.lse_out = lse_out;
   a.lse_blk = nq;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_rows(&tq, q, nq, heads, head_dim) ||
-      !make_tmap_rows_box(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim, fwd_k_box_rows(head_dim)) ||
+  if (!make_tmap_rows(&tq, q, nq, heads, head_dim) || !make_tmap_rows(&tk, k, nk > 0 ? nk : WF_TILE, heads, head_dim) ||
       !make_tmap_rows(&tv, v, nk > 0 ? nk : WF_TILE, heads, head_dim))
     return set_err(WF_ERR_ARG, "wf_block_fwd: TMA map encode failed (alignment?)");
   cudaError_t e = launch_block_fwd(tq, tk, tv, a, head_dim, static_cast<cudaStream_t>(stream));

@@ -169,8 +169,6 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn);
 cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s);
 
-// rows of the K map box launch_block_fwd expects for this head dim (make_tmap_rows_box)
-int fwd_k_box_rows(int D);
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);
 cudaError_t launch_block_bwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,

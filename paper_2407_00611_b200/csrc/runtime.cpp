@@ -837,8 +837,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
         fa.lse_out = b.lse_state + jm * h * n;
         fa.lse_blk = g.n;
         CUtensorMap tq, tk, tv;
-        if (!make_tmap_rows(&tq, qp, fa.nq, g.h, g.d) ||
-            !make_tmap_rows_box(&tk, kp, fa.nk, g.h, g.d, fwd_k_box_rows(g.d)) ||
+        if (!make_tmap_rows(&tq, qp, fa.nq, g.h, g.d) || !make_tmap_rows(&tk, kp, fa.nk, g.h, g.d) ||
             !make_tmap_rows(&tv, vp, fa.nk, g.h, g.d))
           return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
         WCK(dbg_fwd(ctx, fa, qp, kp, vp, E));
@@ -952,8 +951,7 @@ wf_status forward(wf_ctx* ctx, const Geo& g, const bf16* Q, const bf16* K, const
       }
       if (ctx->dry) return WF_OK;
       CUtensorMap tq, tk, tv;
-      if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) ||
-          !make_tmap_rows_box(&tk, slot_k(r, s), a.nk, g.h, g.d, fwd_k_box_rows(g.d)) ||
+      if (!make_tmap_rows(&tq, qteam(r), a.nq, g.h, g.d) || !make_tmap_rows(&tk, slot_k(r, s), a.nk, g.h, g.d) ||
           !make_tmap_rows(&tv, slot_v(r, s), a.nk, g.h, g.d))
         return fail(ctx, WF_ERR_ARG, "TMA map encode failed (alignment?)");
       WCK(dbg_fwd(ctx, a, qteam(r), slot_k(r, s), slot_v(r, s), E));
