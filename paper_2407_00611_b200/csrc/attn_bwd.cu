@@ -194,13 +194,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idSP = idesc_bf16_f32(128, 128, 0, 0);   // K x Q^T, V x dO^T (both K-major)
       constexpr uint32_t idKV = idesc_bf16_f32(128, DP, 0, 1);    // P^T (TMEM) / dS^T (smem) x dO / Q (MN-major)
       constexpr uint32_t idQ = idesc_bf16_f32(128, DP, 1, 1);     // dS (smem, MN-major) x K (MN-major)
-      const uint32_t sK = smem_u32(smem + Cfg::OFF_K);
-      const uint32_t sV = smem_u32(smem + Cfg::OFF_V);
-      const uint32_t sDO = smem_u32(smem + Cfg::OFF_DO);
-      const uint32_t sDS = smem_u32(smem + Cfg::OFF_DS);
+      // descriptor low words (desc_lo): K-major operands with LBO 16, MN-major with LBO = PANEL
+      const uint32_t kK = desc_lo(smem_u32(smem + Cfg::OFF_K), 16);
+      const uint32_t kKm = desc_lo(smem_u32(smem + Cfg::OFF_K), Cfg::PANEL);
+      const uint32_t kV = desc_lo(smem_u32(smem + Cfg::OFF_V), 16);
+      const uint32_t kDO = desc_lo(smem_u32(smem + Cfg::OFF_DO), 16);
+      const uint32_t kDOm = desc_lo(smem_u32(smem + Cfg::OFF_DO), Cfg::PANEL);
+      const uint32_t kDS = desc_lo(smem_u32(smem + Cfg::OFF_DS), 16);
+      const uint32_t kDSm = desc_lo(smem_u32(smem + Cfg::OFF_DS), Cfg::PANEL);
       auto issue_s = [&](int i) {
         const int st = i % QST;
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
+        const uint32_t kQ = desc_lo(smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE), 16);
         tl_stamp(a.tl, tlon, 0, i, 4);
         if (kPark && i >= 2) mbar_wait(&bar[B_SRF], (i - 2) & 1);  // drain of tile i-2 left S^T columns [64, 128)
         mbar_wait(&bar[B_QF + st], (i / QST) & 1);
@@ -209,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
           const int p = k >> 2, kk = k & 3;
-          mma_ss(tbase + 0, smem_desc_sw128(sK + p * Cfg::PANEL + kk * 32, 16, 1024),
-                 smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024), idSP, k > 0 ? 1u : 0u);
+          const uint32_t off = (p * Cfg::PANEL + kk * 32) >> 4;
+          mma_ss_lo(tbase + 0, kK + off, kQ + off, idSP, k > 0 ? 1u : 0u);
         }
         mma_commit(&bar[B_S]);
       };
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ntiles > 0) issue_s(0);
       for (int ii = 0; ii < ntiles; ++ii) {
         const int st = ii % QST;
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE);
+        const uint32_t kQm = desc_lo(smem_u32(smem + Cfg::OFF_Q + st * Cfg::TILE), Cfg::PANEL);
         // dP^T = V dO^T (the dP region must be drained of the previous dQ)
         tl_stamp(a.tl, tlon, 0, ii, 6);
         mbar_wait(&bar[B_DOF], ii & 1);
@@ -231,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
           const int p = k >> 2, kk = k & 3;
-          mma_ss(tbase + 256, smem_desc_sw128(sV + p * Cfg::PANEL + kk * 32, 16, 1024),
-                 smem_desc_sw128(sDO + p * Cfg::PANEL + kk * 32, 16, 1024), idSP, k > 0 ? 1u : 0u);
+          const uint32_t off = (p * Cfg::PANEL + kk * 32) >> 4;
+          mma_ss_lo(tbase + 256, kV + off, kDO + off, idSP, k > 0 ? 1u : 0u);
         }
         mma_commit(&bar[B_DP]);
         // dV += P^T dO
@@ -241,8 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tl_stamp(a.tl, tlon, 0, ii, 1);
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
-          mma_ts(tbase + 128, tbase + 0 + k * 8, smem_desc_sw128(sDO + k * 2048, Cfg::PANEL, 1024), idKV,
-                 (ii > 0 || k > 0) ? 1u : 0u);
+          mma_ts_lo(tbase + 128, tbase + 0 + k * 8, kDOm + k * 128, idKV, (ii > 0 || k > 0) ? 1u : 0u);
         mma_commit(&bar[B_DOE]);
         if (ii + 1 < ntiles) issue_s(ii + 1);
         tl_stamp(a.tl, tlon, 0, ii, 2);
@@ -252,13 +255,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tl_stamp(a.tl, tlon, 0, ii, 3);
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
-          mma_ss(tbase + 256, smem_desc_sw128(sDS + k * 2048, Cfg::PANEL, 1024),
-                 smem_desc_sw128(sK + k * 2048, Cfg::PANEL, 1024), idQ, k > 0 ? 1u : 0u);
+          mma_ss_lo(tbase + 256, kDSm + k * 128, kKm + k * 128, idQ, k > 0 ? 1u : 0u);
         mma_commit(&bar[B_DQF]);
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
-          mma_ss(tbase + 384, smem_desc_sw128(sDS + (k >> 2) * Cfg::PANEL + (k & 3) * 32, 16, 1024),
-                 smem_desc_sw128(sQ + k * 2048, Cfg::PANEL, 1024), idKV, (ii > 0 || k > 0) ? 1u : 0u);
+          mma_ss_lo(tbase + 384, kDS + (((k >> 2) * Cfg::PANEL + (k & 3) * 32) >> 4), kQm + k * 128, idKV,
+                    (ii > 0 || k > 0) ? 1u : 0u);
         mma_commit(&bar[B_QE + st]);
         mma_commit(&bar[B_DSE]);
       }

@@ -184,15 +184,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);  // Q (K-major) x K (K-major)
       constexpr uint32_t idO = idesc_bf16_f32(128, DP, 0, 1);   // P (TMEM) x V (MN-major)
+      // descriptor low words (desc_lo), hoisted out of the issue loops
+      const uint32_t kQ = desc_lo(smem_u32(smem + Cfg::OFF_Q), 16);
+      const uint32_t kK = desc_lo(smem_u32(smem + Cfg::OFF_K), 16);
+      const uint32_t kV = desc_lo(smem_u32(smem + Cfg::OFF_V), Cfg::PANEL);
       auto issue_s = [&](int t, int j) {
         const int st = j % kKStages;
-        const uint32_t sQ = smem_u32(smem + Cfg::OFF_Q + t * Cfg::TILE);
-        const uint32_t sK = smem_u32(smem + Cfg::OFF_K + st * Cfg::TILE);
+        const uint32_t q = kQ + ((t * Cfg::TILE) >> 4), kt = kK + ((st * Cfg::TILE) >> 4);
 #pragma unroll
         for (int k = 0; k < DP / 16; ++k) {
-          const int p = k >> 2, kk = k & 3;
-          mma_ss(tbase + t * 128, smem_desc_sw128(sQ + p * Cfg::PANEL + kk * 32, 16, 1024),
-                 smem_desc_sw128(sK + p * Cfg::PANEL + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+          const uint32_t off = ((k >> 2) * Cfg::PANEL + (k & 3) * 32) >> 4;
+          mma_ss_lo(tbase + t * 128, q + off, kt + off, idS, k > 0 ? 1u : 0u);
         }
         mma_commit(&bar[B_S + t]);
       };
@@ -201,11 +203,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&bar[B_P + 4 * t], j & 1);
         if (t == 0) mbar_wait(&bar[B_V + st], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t sV = smem_u32(smem + Cfg::OFF_V + st * Cfg::TILE);
+        const uint32_t vt = kV + ((st * Cfg::TILE) >> 4);
+        const uint32_t acc0 = (j > 0 || has_state) ? 1u : 0u;
 #pragma unroll
         for (int k = 0; k < WF_TILE / 16; ++k)
-          mma_ts(tbase + 256 + t * 128, tbase + t * 128 + k * 8, smem_desc_sw128(sV + k * 2048, Cfg::PANEL, 1024),
-                 idO, (j > 0 || has_state || k > 0) ? 1u : 0u);
+          mma_ts_lo(tbase + 256 + t * 128, tbase + t * 128 + k * 8, vt + k * 128, idO, k > 0 ? 1u : acc0);
       };
       const int nvis = kv_iter().count(a.kpos);
       mbar_wait(&bar[B_Q], 0);

@@ -246,6 +246,38 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
   d |= static_cast<uint64_t>(2) << 61;  // layout = SWIZZLE_128B
   return d;
 }
+// The same descriptor split in 32-bit halves for the MMA issue loops.  With SBO = 1024 B the
+// high word is a constant; the low word is (address >> 4) | (LBO >> 4) << 16, and since
+// shared addresses stay below 2^18 the descriptor of (address + offset) is low word +
+// offset / 16.  A 128x128x16 `tcgen05.mma` executes in 64 cycles, and the single issuing
+// thread must keep up: tools/mma_rate.cu measures back-to-back MMAs at exactly that floor
+// with hoisted descriptors, and at ~97 cycles each when every descriptor is rebuilt from
+// its address inside a rolled loop (shift, mask, or, 64-bit packing).
+constexpr uint32_t kDescHiSw128 = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+  return (saddr >> 4) | ((lbo_bytes >> 4) << 16);
+}
+__device__ __forceinline__ void mma_ss_lo(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 da, {%1, %5};\n\tmov.b64 db, {%2, %5};\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(kDescHiSw128)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_lo(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 db;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(kDescHiSw128)
+      : "memory");
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B, fp32 D.
 //   a_mn/b_mn: 1 if the operand is MN-major (transposed), 0 if K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, int a_mn, int b_mn) {
