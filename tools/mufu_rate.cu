@@ -1,0 +1,116 @@
+// GPU-box microbenchmark: exponentials per cycle per SM of ex2.approx.ftz.f32 against
+// ex2.approx.f16x2 (two results per instruction), 8 independent chains per thread; then the
+// bf16x2 pack (cvt.rn.bf16x2.f32, F2FP) alone and interleaved with the exponentials, to see
+// whether the pack shares the MUFU (XU) pipe.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/mufu_rate.cu -o /tmp/mufu_rate && /tmp/mufu_rate
+#include <cstdint>
+#include <cstdio>
+#include <cuda_fp16.h>
+
+constexpr int kIters = 4096;
+
+template <bool F16>
+__global__ void __launch_bounds__(512) mufu(float seed, unsigned long long* cyc, float* sink) {
+  float acc = 0.f;
+  unsigned long long t0 = clock64();
+  if (F16) {
+    uint32_t v[8];
+    for (int k = 0; k < 8; ++k) {
+      __half2 h = __floats2half2_rn(-seed * (k + 1) * 1e-3f, -seed * (k + 2) * 1e-3f);
+      v[k] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    for (int i = 0; i < kIters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v[k]));
+    for (int k = 0; k < 8; ++k) {
+      const __half2 h = *reinterpret_cast<__half2*>(&v[k]);
+      acc += __low2float(h) + __high2float(h);
+    }
+  } else {
+    float v[8];
+    for (int k = 0; k < 8; ++k) v[k] = -seed * (k + 1) * 1e-3f;
+    for (int i = 0; i < kIters; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[k]));
+    for (int k = 0; k < 8; ++k) acc += v[k];
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+  if (acc == 12345.f) *sink = acc;
+}
+
+// kind 0: F2FP packs only; kind 1: 2 exponentials + 1 pack per pair (the softmax mix);
+// kind 2: 2 exponentials + integer round-and-permute pack (2 IADD + PRMT, no F2FP)
+template <int KIND>
+__global__ void __launch_bounds__(512) packmix(float seed, unsigned long long* cyc, float* sink) {
+  float v[8];
+  uint32_t acc = 0;
+  for (int k = 0; k < 8; ++k) v[k] = -seed * (k + 1) * 1e-3f;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      float a = v[k], b = v[k + 1];
+      if (KIND > 0) {
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(b));
+      }
+      uint32_t pk;
+      if (KIND < 2) {
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(b), "f"(a));
+      } else {
+        const uint32_t ua = __float_as_uint(a) + 0x8000u, ub = __float_as_uint(b) + 0x8000u;
+        asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(pk) : "r"(ua), "r"(ub));
+      }
+      acc ^= pk;
+      v[k] = a + __uint_as_float(pk & 1u);
+      v[k + 1] = b;
+    }
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+  if (acc == 12345u) *sink = v[0];
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unsigned long long* d;
+  float* s;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&s, 4);
+  for (int threads : {128, 256, 512}) {
+    for (int f16 = 0; f16 < 2; ++f16) {
+      for (int it = 0; it < 2; ++it) {
+        if (f16)
+          mufu<true><<<sms, threads>>>(1.f, d, s);
+        else
+          mufu<false><<<sms, threads>>>(1.f, d, s);
+      }
+      cudaDeviceSynchronize();
+      unsigned long long c;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      const double instr = double(kIters) * 8 * threads;  // warp-lane instructions per SM
+      const double results = instr * (f16 ? 2 : 1);
+      printf("%s threads/SM %d: %.2f instr/clk/SM, %.2f exponentials/clk/SM\n", f16 ? "ex2.f16x2" : "ex2.f32  ", threads,
+             instr / c, results / c);
+    }
+  }
+  for (int kind = 0; kind < 3; ++kind) {
+    const int threads = 256;
+    for (int it = 0; it < 2; ++it) {
+      if (kind == 0) packmix<0><<<sms, threads>>>(1.f, d, s);
+      if (kind == 1) packmix<1><<<sms, threads>>>(1.f, d, s);
+      if (kind == 2) packmix<2><<<sms, threads>>>(1.f, d, s);
+    }
+    cudaDeviceSynchronize();
+    unsigned long long c;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    const double pairs = double(kIters) * 4 * threads;
+    printf("%s: %.2f pairs/clk/SM (%.2f exponentials/clk/SM)\n",
+           kind == 0 ? "F2FP pack only          " : (kind == 1 ? "2 ex2 + F2FP pack       " : "2 ex2 + IADD/PRMT pack  "),
+           pairs / c, kind ? 2 * pairs / c : 0.0);
+  }
+  return 0;
+}
