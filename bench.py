@@ -186,11 +186,34 @@ def run_reference(args):
            "config": config_of(name, N, heads, hd, causal, P),
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
     return 0
 
 
+_RESULT_FD = None
+
+
+def _keep_stdout_for_result():
+    """Route everything written to fd 1 (NCCL's version banner, library prints) to stderr so
+    that stdout carries exactly the one JSON result line."""
+    global _RESULT_FD
+    if _RESULT_FD is None:
+        sys.stdout.flush()
+        _RESULT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(out):
+    line = json.dumps(out) + "\n"
+    if _RESULT_FD is None:
+        sys.stdout.write(line)
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, line.encode())
+
+
 def main():
+    _keep_stdout_for_result()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -458,7 +481,7 @@ def main():
         out["e2e"] = head_rec.get("e2e")
         out["gpu_launches"] = head_rec["gpu_launches"]
         out["clocks"] = head_rec["clocks"]
-        print(json.dumps(out), flush=True)
+        emit(out)
     if world > 1:
         dist.destroy_process_group()
     return 0
