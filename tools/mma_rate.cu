@@ -138,6 +138,23 @@ __global__ void __launch_bounds__(256, 1) mma_rate(int mode, int bg, unsigned lo
       }
       if (blockIdx.x == 0) out[2] = n;
     }
+  } else if (warp >= 2 && bg == 4) {
+    // six warps of softmax-like work: packed FMAs, exponentials, bf16 packs (ALU/FMA/MUFU)
+    float2 x = make_float2(threadIdx.x * 1e-3f, -threadIdx.x * 1e-3f);
+    uint32_t acc = 0;
+    unsigned long long n = 0;
+    while (!done) {
+#pragma unroll 16
+      for (int i = 0; i < 64; ++i) {
+        const float2 y = ffma2(x, make_float2(0.999f, 0.999f), make_float2(-1e-4f, 1e-4f));
+        const float2 p = make_float2(fast_exp2(y.x), fast_exp2(y.y));
+        acc ^= pack_bf16x2(p.x, p.y);
+        x = fadd2(y, make_float2(p.x * 1e-6f, p.y * 1e-6f));
+      }
+      ++n;
+    }
+    if (acc == 0x12345u) out[3] = n;
+    if (blockIdx.x == 0 && lane == 0 && warp == 4) out[2] = n;
   } else if (warp >= 4 && bg && bg < 3) {
     const uint32_t tl = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     unsigned long long n = 0;
@@ -183,7 +200,7 @@ void run(int mode, int bg, int sms) {
   cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
   printf("N=%d mode %2d %s%s%s bg=%s: issue %.1f cyc/mma, complete %.1f cyc/mma (floor %d), %.1f ns/mma = %.0f MHz, bg iters %llu %s\n",
  N, mode, mode >= 8 ? "groups" : ((mode & 1) ? "TS" : "SS"), (mode < 8 && (mode & 4)) ? " A-MN" : "",
-         (mode < 8 && (mode & 2)) ? " B-MN" : "", bg == 0 ? "none" : (bg == 1 ? "tmem-ld" : (bg == 2 ? "tmem-st" : "tma-load")), double(h[0]) / kMmas,
+         (mode < 8 && (mode & 2)) ? " B-MN" : "", bg == 0 ? "none" : (bg == 1 ? "tmem-ld" : (bg == 2 ? "tmem-st" : (bg == 3 ? "tma-load" : "softmax-like"))), double(h[0]) / kMmas,
          double(h[1]) / kMmas, 128 * N / 256, double(h[4]) / kMmas, 1e3 * double(h[1]) / double(h[4]), h[2],
          e == cudaSuccess ? "" : cudaGetErrorString(e));
   cudaFree(d);
@@ -199,5 +216,11 @@ int main() {
       run<256>(mode, bg, sms);
     }
   for (int mode = 8; mode < 17; ++mode) run<128>(mode, 0, sms);
+  for (int mode : modes) run<64>(mode, 0, sms);  // N = 64 (the 64-key sub-tile S)
+  for (int mode : {0, 1}) {  // with softmax-like compute on six other warps
+    run<128>(mode, 4, sms);
+    run<64>(mode, 4, sms);
+  }
+  for (int mode = 8; mode < 10; ++mode) run<128>(mode, 4, sms);
   return 0;
 }
