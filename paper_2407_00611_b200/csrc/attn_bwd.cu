@@ -50,9 +50,6 @@ enum {
 #ifndef WF_BWD_POLY_EVERY
 #define WF_BWD_POLY_EVERY 0  // every k-th exponential pair of the P phase on the FMA pipe
 #endif
-#ifndef WF_DQ_ATOMIC
-#define WF_DQ_ATOMIC 0
-#endif
 constexpr int kThreads = 14 * 32;  // 4 dQ-drain + 8 compute + TMA + MMA warps
 constexpr int kCompute = 256;
 
@@ -434,7 +431,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // second half is read) -> this warp's double-buffered staging boxes [32 rows][32 fp32]
     // (128B swizzle, 16-byte chunk j at j ^ (row & 7): conflict-free) -> one TMA tensor
     // reduce-add per box into the fp32 dQ accumulator.
-    const int r = warp * 32 + lane;  // query row within the tile
     const uint32_t tl = tbase + (static_cast<uint32_t>(warp * 32) << 16);
     uint8_t* wbox0 = smem + Cfg::OFF_STG + warp * 8192;
     const int ntiles = q_iter().count(a.qpos);
@@ -508,17 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (sub == 1 && !two) break;
             const int c0 = cbase + 32 * sub;
             const uint32_t* rr = sub == 0 ? ra : rb;
-#if WF_DQ_ATOMIC
-            // experiment: vector reductions straight from registers (no shared memory)
-            float* dst = a.dq_acc + (static_cast<size_t>(it * WF_TILE + r) * a.heads + head) * D + c0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (c0 + 4 * j < D)
-                atomicAdd(reinterpret_cast<float4*>(dst) + j,
-                          make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
-                                      __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3])));
-            (void)wbox0;
-#else
             uint8_t* wbox = wbox0 + (chunk & 1) * 4096;
             if (lane == 0) bulk_wait_read<1>();  // the reduce of chunk-2 has read this box
             __syncwarp();
@@ -532,7 +517,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_reduce_add_3d(&tmDQ, wbox, c0, head, it * WF_TILE + warp * 32);
               bulk_commit();
             }
-#endif
             ++chunk;
           }
         }
