@@ -240,7 +240,7 @@ extern "C" wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int 
   const bool oka = a_mn ? make_tmap_2d(&ta, A, K, M, 64) : make_tmap_2d(&ta, A, M, K, 128);
   const bool okb = b_mn ? make_tmap_2d(&tb, B, K, N, 64) : make_tmap_2d(&tb, B, N, K, pair ? 128 : bn);
   if (!oka || !okb) return set_err(WF_ERR_ARG, "wf_gemm_bf16: TMA map encode failed");
-  cudaError_t e = pair ? launch_gemm_pair(ta, tb, g, static_cast<cudaStream_t>(stream))
+  cudaError_t e = pair ? launch_gemm_pair(ta, tb, g, a_mn ? 1 : 0, b_mn ? 1 : 0, static_cast<cudaStream_t>(stream))
                        : launch_gemm_t(ta, tb, g, bn, a_mn ? 1 : 0, b_mn ? 1 : 0, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(WF_ERR_CUDA, cudaGetErrorString(e));
   return WF_OK;

@@ -167,7 +167,9 @@ cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 // CTA-pair (cta_group::2) variant for K-major A and B with M, N, split multiples of 256
 // (used whenever it applies); its A and B maps both use 128-row boxes.
 bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn);
-cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s);
+// CTA-pair GEMM (256 x 256 tiles) for any operand layout; requires gemm_pair_ok
+cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int a_mn, int b_mn,
+                             cudaStream_t s);
 
 cudaError_t launch_block_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const FwdArgs& a,
                              int D, cudaStream_t s);

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------- CTA-pair variant
-// Same contract for K-major A and B, pair tile 256 x 256: the even CTA of a cluster of two
+// Same contract for every operand layout (K- or MN-major A and B), pair tile 256 x 256: the even CTA of a cluster of two
 // issues M = 256 `tcgen05.mma.cta_group::2` MMAs whose A rows [0, 128) come from its own
 // shared memory and [128, 256) from its peer's, with the 256 N rows of B split 128 / 128;
 // each CTA loads half of both operand tiles and receives its 128 output rows x 256 columns
@@ -211,6 +211,7 @@ struct Gemm2Cfg {
 };
 enum { P_FULL = 0, P_EMPTY = 6, P_TFULL = 12, P_TEMPTY = 14, P_NUM = 16 };
 
+template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     wf_gemm2_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                     const __grid_constant__ GemmArgs g) {
@@ -257,14 +258,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (it >= Cfg::ST) mbar_wait(&bar[P_EMPTY + s], ((it / Cfg::ST) - 1) & 1);
           uint8_t* sa = smem + s * Cfg::STAGE;
           if (cr == 0) mbar_arrive_expect_tx(&bar[P_FULL + s], 2 * Cfg::STAGE);
-          tma_load_2d_pair(sa, &tA, &bar[P_FULL + s], kb * 64, m * 256 + cr * 128);
-          tma_load_2d_pair(sa + Cfg::A_BYTES, &tB, &bar[P_FULL + s], kb * 64, n * 256 + cr * 128);
+          // this CTA's 128 rows of A (M) and of B (N); MN-major operands as two 64-column panels
+          if (A_MN) {
+            for (int p = 0; p < 2; ++p)
+              tma_load_2d_pair(sa + p * 8192, &tA, &bar[P_FULL + s], m * 256 + cr * 128 + p * 64, kb * 64);
+          } else {
+            tma_load_2d_pair(sa, &tA, &bar[P_FULL + s], kb * 64, m * 256 + cr * 128);
+          }
+          if (B_MN) {
+            for (int p = 0; p < 2; ++p)
+              tma_load_2d_pair(sa + Cfg::A_BYTES + p * 8192, &tB, &bar[P_FULL + s], n * 256 + cr * 128 + p * 64,
+                               kb * 64);
+          } else {
+            tma_load_2d_pair(sa + Cfg::A_BYTES, &tB, &bar[P_FULL + s], kb * 64, n * 256 + cr * 128);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (cr == 0 && lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(256, 256, 0, 0);
+      constexpr uint32_t idesc = idesc_bf16_f32(256, 256, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int it = 0, lt = 0;
       for (int tile = cid; tile < ntiles; tile += ncl, ++lt) {
         const int b = lt & 1;
@@ -277,9 +290,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * Cfg::STAGE), sb = sa + Cfg::A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma2_ss(acc, smem_desc_sw128(sa + kk * 32, 16, 1024), smem_desc_sw128(sb + kk * 32, 16, 1024), idesc,
-                    (kb | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t da = A_MN ? smem_desc_sw128(sa + kk * 2048, 8192, 1024) : smem_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? smem_desc_sw128(sb + kk * 2048, 8192, 1024) : smem_desc_sw128(sb + kk * 32, 16, 1024);
+            mma2_ss(acc, da, db, idesc, (kb | kk) ? 1u : 0u);
+          }
           mma2_commit_mc(&bar[P_EMPTY + s], 0x3);
         }
         mma2_commit_mc(&bar[P_TFULL + b], 0x3);
@@ -382,21 +397,33 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Gemm
   return launch_gemm_t(ta, tb, g, bn, 0, 0, s);
 }
 
-bool gemm_pair_ok(const GemmArgs& g, int a_mn, int b_mn) {
-  return !a_mn && !b_mn && g.M % 256 == 0 && g.N % 256 == 0 && g.split % 256 == 0;
+bool gemm_pair_ok(const GemmArgs& g, int /*a_mn*/, int /*b_mn*/) {
+  return g.M % 256 == 0 && g.N % 256 == 0 && g.split % 256 == 0;
 }
 
-cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+namespace {
+template <bool A_MN, bool B_MN>
+cudaError_t launch_pair_layout(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(wf_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(wf_gemm2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Gemm2Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int ntiles = (g.M / 256) * (g.N / 256);
   const int pairs = ntiles < sm_count() / 2 ? ntiles : sm_count() / 2;
-  wf_gemm2_kernel<<<2 * pairs, 192, Gemm2Cfg::SMEM, s>>>(ta, tb, g);
+  wf_gemm2_kernel<A_MN, B_MN><<<2 * pairs, 192, Gemm2Cfg::SMEM, s>>>(ta, tb, g);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int a_mn, int b_mn,
+                             cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_pair_layout<false, false>(ta, tb, g, s);
+  if (!a_mn && b_mn) return launch_pair_layout<false, true>(ta, tb, g, s);
+  if (a_mn && b_mn) return launch_pair_layout<true, true>(ta, tb, g, s);
+  return launch_pair_layout<true, false>(ta, tb, g, s);
 }
 
 cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn, int a_mn, int b_mn,

@@ -1694,7 +1694,7 @@ wf_status wf_qkv_proj(wf_ctx* ctx, const void* X, const void* W, int64_t N, int 
     CUtensorMap tx;
     if (!make_tmap_2d(&tx, static_cast<const bf16*>(X) + ro * n * hidden, n, hidden, 128))
       return fail(ctx, WF_ERR_ARG, "wf_qkv_proj: TMA map encode failed");
-    WCK(kcheck(ctx, pair ? launch_gemm_pair(tx, tw, ga, st) : launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
+    WCK(kcheck(ctx, pair ? launch_gemm_pair(tx, tw, ga, 0, 0, st) : launch_gemm(tx, tw, ga, bn, st), "qkv_gemm"));
   }
   if (fuse) {
     ctx->proj_seq = ctx->seq;

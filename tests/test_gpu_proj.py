@@ -42,7 +42,7 @@ def test_gemm_parity(M, N, K):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (1, 1), (1, 0)])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 192), (384, 1152, 256)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 192), (384, 1152, 256), (512, 768, 320), (1024, 512, 4096)])
 def test_gemm_transposed_layouts(a_mn, b_mn, M, N, K):
     # the backward products of a projection: dX = dY W (b_mn), dW = dY^T X (a_mn, b_mn)
     wf = _wf()
