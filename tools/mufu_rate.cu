@@ -73,6 +73,46 @@ __global__ void __launch_bounds__(512) packmix(float seed, unsigned long long* c
   if (acc == 12345u) *sink = v[0];
 }
 
+// the softmax / P-phase mix: per pair one packed FFMA2 (scale, minus the row statistic read
+// from shared memory as a broadcast float2), two MUFU.EX2, one F2FP pack (+ optionally an
+// FADD2 row sum), 32 pairs per thread per "tile" from registers, as the block kernels do
+template <bool SUM>
+__global__ void __launch_bounds__(512) softmax_mix(float seed, unsigned long long* cyc, float* sink) {
+  __shared__ float2 stat[64];
+  if (threadIdx.x < 64) stat[threadIdx.x] = make_float2(-seed * threadIdx.x * 1e-3f, -seed * 1e-3f);
+  __syncthreads();
+  float sv[64];
+  for (int i = 0; i < 64; ++i) sv[i] = (threadIdx.x + i) * 1e-3f;
+  uint32_t acc = 0;
+  float2 rs = make_float2(0.f, 0.f);
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < 256; ++it) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 st = stat[(i + it) & 63];
+      float2 x;
+      asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+          "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %6};\n\t"
+          "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+          : "=f"(x.x), "=f"(x.y)
+          : "f"(sv[2 * i]), "f"(sv[2 * i + 1]), "f"(0.0884f), "f"(st.x), "f"(st.y));
+      float e0, e1;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(x.x));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(x.y));
+      uint32_t pk;
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(e1), "f"(e0));
+      acc ^= pk;
+      if (SUM) {
+        rs.x += e0;
+        rs.y += e1;
+      }
+    }
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+  if (acc == 12345u || rs.x == 1.2345f) *sink = rs.y;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -111,6 +151,21 @@ int main() {
     printf("%s: %.2f pairs/clk/SM (%.2f exponentials/clk/SM)\n",
            kind == 0 ? "F2FP pack only          " : (kind == 1 ? "2 ex2 + F2FP pack       " : "2 ex2 + IADD/PRMT pack  "),
            pairs / c, kind ? 2 * pairs / c : 0.0);
+  }
+  for (int threads : {128, 256, 512}) {
+    for (int sum = 0; sum < 2; ++sum) {
+      for (int it = 0; it < 2; ++it) {
+        if (sum)
+          softmax_mix<true><<<sms, threads>>>(1.f, d, s);
+        else
+          softmax_mix<false><<<sms, threads>>>(1.f, d, s);
+      }
+      cudaDeviceSynchronize();
+      unsigned long long c;
+      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      const double exps = 256.0 * 64 * threads;
+      printf("softmax mix%s, %d threads/SM: %.2f exponentials/clk/SM\n", sum ? " + row sum" : "", threads, exps / c);
+    }
   }
   return 0;
 }
