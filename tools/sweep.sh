@@ -15,7 +15,7 @@ for C in 1 2 4; do
   run $C gpt 0
   run $C dit 0
 done
-for N in 16384 65536 262144 524288; do
+for N in 16384 65536 131072 262144 524288; do
   run 1 gpt $N
   run $NG gpt $N
 done
