@@ -241,8 +241,8 @@ wf_status wf_gemm_bf16_t(const void* A, int a_mn, const void* B, int b_mn, int M
  *   dx = rstd (g - mean(g) - xhat mean(g o xhat)) (+ dres if non-NULL: the residual
  *   branch's gradient); dw += sum_rows dy o xhat, db += sum_rows dy (fp32 [hidden],
  *   accumulated: zero them first).
- * wf_gelu_fwd: h = u Phi(u) elementwise (exact erf GELU, the FeedForward activation);
- *   n elements, n % 8 == 0.
+ * wf_gelu_fwd: h = u Phi(u) elementwise (exact erf GELU, the FeedForward activation; erf
+ *   evaluated to |error| <= 1.5e-7, Abramowitz & Stegun 7.1.26); n elements, n % 8 == 0.
  * wf_gelu_bwd: du = dh o (Phi(u) + u phi(u)).
  * wf_add_bf16: y = a + b (n elements, n % 8 == 0).
  * wf_pack3_bf16: y [rows, 3E] = [a | b | c] (a, b, c [rows, E]). */

@@ -2,8 +2,9 @@
 // item 3; "finalized after a standard LayerNorm and FeedForward layer process"):
 // LayerNorm forward/backward, the FeedForward layer's GELU forward/backward, the residual
 // add and the packing of (dQ, dK, dV) into one [rows, 3E] operand for the projection's
-// backward GEMMs.  All HBM-bound: 16-byte vector accesses, one CTA per row for the
-// normalisations (a row is 8 KB at hidden 4096).
+// backward GEMMs.  All HBM-bound: 16-byte vector accesses; the normalisations run one CTA
+// (256 threads) per row at a time, persistent CTAs walking the rows with the next row's
+// loads in flight (a row is 8 KB at hidden 4096).
 #include <cstdint>
 #include <cstdio>
 
