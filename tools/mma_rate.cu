@@ -206,6 +206,8 @@ void run(int mode, int bg, int sms) {
   cudaFree(d);
 }
 
+int main_pair();
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -222,5 +224,101 @@ int main() {
     run<64>(mode, 4, sms);
   }
   for (int mode = 8; mode < 10; ++mode) run<128>(mode, 4, sms);
+  main_pair();
+  return 0;
+}
+
+// ---------------------------------------------------------------- CTA-pair (cta_group::2)
+// The even CTA of a cluster of two issues M = 256 MMAs (A rows from both CTAs' shared
+// memory, B split along N: each CTA holds N / 2 rows), SS or TS (A from both CTAs' TMEM).
+__device__ __forceinline__ void mma2_ts_rate(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int N, bool TS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma2_rate(unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_ctarank();
+  for (int i = threadIdx.x; i < (16384 + N / 2 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc2(&tslot, 512);
+    tmem_relinquish2();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tb = tslot;
+  if (cr == 0 && warp == 0 && lane == 0) {
+    const uint32_t idesc = idesc_bf16_f32(256, N, 0, 0);
+    const uint32_t sa = smem_u32(smem), sb = sa + 16384;
+    uint64_t da[4], db[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      da[kk] = smem_desc_sw128(sa + kk * 32, 16, 1024);
+      db[kk] = smem_desc_sw128(sb + kk * 32, 16, 1024);
+    }
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < kMmas; i += 4)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (TS)
+          mma2_ts_rate(tb, tb + 256 + kk * 8, db[kk], idesc, 1u);
+        else
+          mma2_ss(tb, da[kk], db[kk], idesc, 1u);
+      }
+    unsigned long long t1 = clock64();
+    mma2_commit_mc(&bar, 0x3);
+    mbar_wait(&bar, 0);
+    unsigned long long t2 = clock64();
+    if (blockIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  } else if (cr == 1 && threadIdx.x == 0) {
+    mbar_wait(&bar, 0);  // the multicast commit
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0) tmem_dealloc2(tb, 512);
+}
+
+template <int N, bool TS>
+void run2(int sms) {
+  unsigned long long* d;
+  cudaMalloc(&d, 64);
+  cudaMemset(d, 0, 64);
+  const int sm = 16384 + N / 2 * 128 + 1024;
+  cudaFuncSetAttribute(mma2_rate<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  for (int it = 0; it < 3; ++it) mma2_rate<N, TS><<<sms, 128, sm>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[2];
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("pair M=256 N=%d %s: issue %.1f cyc/mma, complete %.1f cyc/mma (floor per SM %d) %s\n", N, TS ? "TS" : "SS",
+         double(h[0]) / kMmas, double(h[1]) / kMmas, 256 * N / 512, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main_pair() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  sms &= ~1;
+  run2<128, false>(sms);
+  run2<128, true>(sms);
+  run2<256, false>(sms);
+  run2<256, true>(sms);
   return 0;
 }
